@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark of the rangekit hot path on B200 (BASELINE.json metric:
+"ICP registrations/sec (64x1024 pairs) and TSDF frames/sec @5cm, % HBM roofline").
+
+One step =
+  (a) ICP: C4 -- a batch of 65,536 independent 64x1024 scan pairs (strong
+      scaling: each of N ranks registers its contiguous 65,536/N slice), drawn
+      from a device-rendered pool of 2,048 unique street pairs; K1 normals of
+      every pool destination + one K3 launch running the full multi-scale
+      schedule (4:20, 2:20, 1:10, early exit) for every pair;
+  (b) TSDF: C2 -- the 100-frame 64x1024 street sequence integrated at 5 cm
+      voxels (tau 0.2 m, max_weight 100, clip 30 m) into a freshly cleared grid.
+``value`` is (a) in registrations/s over all ranks; (b) is reported under
+"tsdf".  Inputs live in HBM before the timed region; the ICP pool (>3 GB) is
+far larger than the 126 MB L2.  ``e2e`` repeats (a)+(b) through the public API
+with pinned-host inputs copied in and poses / voxel counts copied out inside
+the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ICP registrations/sec (64x1024 pairs) and TSDF frames/sec @5cm, % HBM roofline"
+ICP_BYTES_PER_PT_IT = 20      # src range 4 + dst range 4 + dst normal 12
+TSDF_BYTES_PER_VOXEL = 16     # 8 B read + 8 B write of {tsdf, weight}
+TSDF_BYTES_PER_PIXEL = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pairs", type=int, default=65536)
+    ap.add_argument("--pool", type=int, default=2048)
+    ap.add_argument("--frames", type=int, default=100)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ workloads
+
+def make_inputs(args, rank, world, device):
+    """Render the ICP pool and the TSDF sequence on the device."""
+    import torch
+
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = scenes.ouster64()
+    street = scenes.street_scene()
+    pool = scenes.pair_pool_poses(args.pool, seed=0)
+    dst_poses = [b for b, _ in pool]
+    src_poses = [b @ gt for b, gt in pool]
+    src = pipeline.render_batch(intr, street, src_poses)
+    dst = pipeline.render_batch(intr, street, dst_poses)
+    lo, hi = pipeline.shard(args.pairs, rank, world)
+    # spread concurrent CTAs over different pool images (golden-ratio stride)
+    idx = (np.arange(lo, hi, dtype=np.int64) * 1237) % args.pool
+    pair_idx = torch.from_numpy(idx.astype(np.int32)).to(device)
+    traj = scenes.street_trajectory(args.frames, seed=0)
+    frames = pipeline.render_batch(intr, street, traj)
+    poses_w = torch.from_numpy(pipeline.poses_to_rows(traj)).to(device)
+    inv_w = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).to(device)
+    gts = np.stack([gt.as_row12() for _, gt in pool])
+    torch.cuda.synchronize()
+    return dict(intr=intr, src=src, dst=dst, pair_idx=pair_idx, n_pairs=hi - lo, frames=frames,
+                poses_w=poses_w, inv_w=inv_w, traj=traj, gts=gts)
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    import paper_2112_02779_b200 as rk
+    from paper_2112_02779_b200 import pipeline
+    from paper_2112_02779_b200.range_image import normals_cross_batch
+
+    device = torch.device("cuda", torch.cuda.current_device())
+    D = make_inputs(args, rank, world, device)
+    intr = D["intr"]
+    cfg = rk.RegistrationConfig()
+    grid = rk.VoxelBlockGrid(voxel_size=0.05, capacity=32768)
+    stream = torch.cuda.current_stream()
+    pt_iters = torch.zeros(1, dtype=torch.int64, device=device)
+    updated = torch.zeros(1, dtype=torch.int64, device=device)
+
+    ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for k in ("normals", "icp", "tsdf")}
+    acc = {k: 0.0 for k in ev}
+
+    def step(timed):
+        e = ev["normals"]
+        e[0].record(stream)
+        surf = normals_cross_batch(intr, D["dst"])
+        e[1].record(stream)
+        ev["icp"][0].record(stream)
+        res = rk.register_batch(intr, D["src"], D["dst"], surf, pair_src=D["pair_idx"],
+                                pair_dst=D["pair_idx"], config=cfg, pt_iters=pt_iters if timed else None)
+        ev["icp"][1].record(stream)
+        ev["tsdf"][0].record(stream)
+        pipeline.clear_grid(grid)
+        pipeline.integrate_sequence(grid, intr, D["frames"], D["poses_w"], D["inv_w"], clip_max=30.0,
+                                    updated=updated if timed else None)
+        ev["tsdf"][1].record(stream)
+        return res
+
+    for _ in range(args.warmup):
+        res = step(False)
+    torch.cuda.synchronize()
+    n_blocks, cap, overflow, _ = grid.info()
+    if overflow:
+        raise RuntimeError("TSDF pool overflow in warm-up; raise capacity")
+    # correctness spot check on the bench's own output: recovered gt poses
+    poses = res.poses.cpu().numpy()
+    gts = D["gts"][D["pair_idx"].cpu().numpy()]
+    terr = np.linalg.norm(poses[:, 9:] - gts[:, 9:], axis=1)
+    ok_frac = float(np.mean(terr < 0.05))
+
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+            for k, (a, b) in ev.items():
+                pass
+            torch.cuda.synchronize()
+            for k, (a, b) in ev.items():
+                acc[k] += a.elapsed_time(b)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    elapsed_ms = t0.elapsed_time(t1)
+    if dist is not None:
+        t = torch.tensor([elapsed_ms, acc["icp"] + acc["normals"], acc["tsdf"]], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, icp_ms, tsdf_ms = t.tolist()
+        pt = pt_iters.clone()
+        dist.all_reduce(pt)
+        upd = updated.clone()
+        dist.all_reduce(upd)
+        total_pairs = args.pairs
+    else:
+        icp_ms, tsdf_ms = acc["icp"] + acc["normals"], acc["tsdf"]
+        pt, upd = pt_iters, updated
+        total_pairs = D["n_pairs"]
+    K = args.steps
+    reg_per_s = total_pairs * K / (icp_ms / 1e3)
+    tsdf_fps = args.frames * K * world / (tsdf_ms / 1e3)
+    pt_per_launch = pt.item() / K
+    icp_kernel_ms = acc["icp"] / K
+    achieved = ICP_BYTES_PER_PT_IT * pt_per_launch / (icp_kernel_ms / 1e3) / 1e9
+    upd_per_step = upd.item() / K
+    tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd_per_step + TSDF_BYTES_PER_PIXEL * intr.height * intr.width * args.frames
+    tsdf_achieved = tsdf_bytes / (acc["tsdf"] / K / 1e3) / 1e9
+    launches = K * (1 + 1 + pipeline.LAUNCHES_CLEAR + pipeline.LAUNCHES_PER_FRAME * args.frames)
+    return dict(reg_per_s=reg_per_s, tsdf_fps=tsdf_fps, elapsed_ms=elapsed_ms, icp_ms=icp_ms,
+                tsdf_ms=tsdf_ms, achieved=achieved, pt_per_launch=pt_per_launch,
+                icp_kernel_ms=icp_kernel_ms, normals_ms=acc["normals"] / K,
+                tsdf_achieved=tsdf_achieved, tsdf_updated=upd_per_step, n_blocks=n_blocks,
+                clocks=clocks.summary(), launches=launches, ok_frac=ok_frac, D=D, grid=grid, cfg=cfg)
+
+
+def run_e2e(args, rank, world, dist, D, grid, cfg):
+    """Same step through the public API with host buffers: pinned H2D of the
+    step's input images, D2H of poses/status and the voxel count."""
+    import torch
+
+    import paper_2112_02779_b200 as rk
+    from paper_2112_02779_b200 import pipeline
+    from paper_2112_02779_b200.range_image import normals_cross_batch
+    src_h = D["src"].cpu().pin_memory()
+    dst_h = D["dst"].cpu().pin_memory()
+    frames_h = D["frames"].cpu().pin_memory()
+    intr = D["intr"]
+    h2d = src_h.numel() * 4 + dst_h.numel() * 4 + frames_h.numel() * 4
+    d2h = 0
+
+    def step():
+        nonlocal d2h
+        src = src_h.to("cuda", non_blocking=True)
+        dst = dst_h.to("cuda", non_blocking=True)
+        frames = frames_h.to("cuda", non_blocking=True)
+        surf = normals_cross_batch(intr, dst)
+        res = rk.register_batch(intr, src, dst, surf, pair_src=D["pair_idx"], pair_dst=D["pair_idx"],
+                                config=cfg)
+        pipeline.clear_grid(grid)
+        upd = pipeline.integrate_sequence(grid, intr, frames, D["poses_w"], D["inv_w"], clip_max=30.0)
+        poses = res.poses.cpu()
+        status = res.status.cpu()
+        n = upd.cpu()
+        d2h = poses.numel() * 8 + status.numel() * 4 + n.numel() * 8
+        return poses
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([el], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = t.item()
+    total_pairs = args.pairs if dist is not None else D["n_pairs"]
+    return dict(value=total_pairs * args.steps / el, unit="registrations/s",
+                h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                tsdf_frames_in_step=args.frames, seconds=el)
+
+
+# ------------------------------------------------------------------ CPU oracle
+
+def _cpu_icp_job(seed_pairs):
+    """Worker: oracle normals + register on a few pool pairs (single thread)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import icp as oicp
+    from oracle import image as oimg
+    from oracle import sensor as osens
+    from oracle import synth as osynth
+    from paper_2112_02779_b200 import scenes
+    intr = scenes.ouster64()
+    S = osens.Sensor.from_intrinsics(intr)
+    street = scenes.street_scene()
+    pool = scenes.pair_pool_poses(max(seed_pairs) + 1, seed=0)
+    imgs = []
+    for i in seed_pairs:
+        base, gt = pool[i]
+        s = base @ gt
+        imgs.append((osynth.render(S, street, s.R, s.t), osynth.render(S, street, base.R, base.t)))
+    t0 = time.perf_counter()
+    for src, dst in imgs:
+        vec, valid = oimg.normals_cross(S, dst)
+        oicp.register(S, src, dst, vec, valid, fma="blas")
+    return len(imgs), time.perf_counter() - t0
+
+
+def cpu_icp_baseline(budget_s: float):
+    from concurrent.futures import ProcessPoolExecutor
+    cores = os.cpu_count() or 1
+    # calibrate: one pair on one core
+    n1, t1 = _cpu_icp_job([0])
+    per_worker = max(1, int(budget_s / max(t1, 1e-3) / 2))
+    jobs = [list(range(k * per_worker, (k + 1) * per_worker)) for k in range(cores)]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(cores) as ex:
+        outs = list(ex.map(_cpu_icp_job, jobs))
+    wall = time.perf_counter() - t0
+    done = sum(n for n, _ in outs)
+    busy = max(t for _, t in outs)
+    return dict(value=done / busy, unit="registrations/s", cores=cores, kind="port",
+                sample=f"{done} C4 pool pairs (normals + 3-level register), oracle numpy, "
+                       f"{cores} processes x 1 thread, {busy:.1f} s compute ({wall:.1f} s wall)")
+
+
+def cpu_tsdf_baseline(frames: int = 3):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import sensor as osens
+    from oracle import synth as osynth
+    from oracle import tsdf as otsdf
+    from paper_2112_02779_b200 import scenes
+    intr = scenes.ouster64()
+    S = osens.Sensor.from_intrinsics(intr)
+    traj = scenes.street_trajectory(frames, seed=0)
+    imgs = [osynth.render(S, scenes.street_scene(), p.R, p.t) for p in traj]
+    grid = {}
+    t0 = time.perf_counter()
+    for img, p in zip(imgs, traj):
+        otsdf.integrate_cloud_frame(grid, S, img, p.R, p.t, 0.05, 0.2, clip_max=30.0, fma="blas")
+    dt = time.perf_counter() - t0
+    return dict(value=frames / dt, unit="frames/s", cores=1, kind="port",
+                sample=f"{frames} frames of the C2 street sequence at 5 cm, oracle numpy, 1 thread")
+
+
+# ------------------------------------------------------------------ main
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def profile_traffic(kernel: str):
+    """dram bytes per work unit from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(kernel)
+    return None
+
+
+def dist_init(args):
+    if args.gpus <= 1 or "RANK" not in os.environ:
+        return None, 0, 1
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    return dist, dist.get_rank(), dist.get_world_size()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        icp = cpu_icp_baseline(args.cpu_seconds)
+        line = {"impl": "reference", "metric": METRIC, "value": icp["value"], "unit": "registrations/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * args.pairs / icp["value"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+                "config": {"workload": "C4 65,536 64x1024 street pairs (bounded CPU sample) + C2 TSDF 5 cm",
+                           "pairs": args.pairs},
+                "cpu_baseline": icp, "tsdf": cpu_tsdf_baseline(),
+                "e2e": {"value": icp["value"], "unit": "registrations/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    dist, rank, world = dist_init(args)
+    import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    r = run_ours(args, rank, world, dist)
+    e2e = None if args.no_e2e else run_e2e(args, rank, world, dist, r["D"], r["grid"], r["cfg"])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_icp_baseline(args.cpu_seconds)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peak()
+    tr = profile_traffic("k_register")
+    line = {
+        "metric": METRIC, "value": r["reg_per_s"], "unit": "registrations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["elapsed_ms"] / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (f64 transforms/solve)", "data": "synthetic (device-rendered street scene)",
+        "config": {"workload": "C4: 65,536 independent 64x1024 Ouster-like pairs (pool of "
+                               f"{args.pool} unique street pairs), 3-level ICP 4:20,2:20,1:10 + "
+                               f"C2: {args.frames}-frame 64x1024 street sequence, TSDF 5 cm",
+                   "pairs": args.pairs, "pairs_per_rank": r["D"]["n_pairs"], "pool": args.pool,
+                   "frames": args.frames, "voxel_m": 0.05,
+                   "l2": "inputs > L2 (ICP pool %.1f GB)" % (args.pool * 64 * 1024 * 24 / 1e9),
+                   "parallelism": f"pairs sharded over {world} rank(s)"},
+        "tsdf": {"value": r["tsdf_fps"], "unit": "frames/s", "voxels_updated_per_step": r["tsdf_updated"],
+                 "blocks": r["n_blocks"],
+                 "roofline": {"bound": "hbm", "achieved": r["tsdf_achieved"], "peak": peak, "unit": "GB/s",
+                              "frac": r["tsdf_achieved"] / peak, "traffic": profile_traffic("k_integrate")}},
+        "roofline": {"bound": "hbm", "kernel": "k_register", "achieved": r["achieved"], "peak": peak,
+                     "unit": "GB/s", "frac": r["achieved"] / peak,
+                     "traffic": (tr * r["pt_per_launch"] if tr else None),
+                     "work": f"{r['pt_per_launch']:.4g} source-point-iterations x {ICP_BYTES_PER_PT_IT} B "
+                             f"per launch, {r['icp_kernel_ms']:.2f} ms/launch", "peak_source": peak_src},
+        "phase_ms": {"normals": r["normals_ms"], "register": r["icp_kernel_ms"],
+                     "tsdf_sequence": r["tsdf_ms"] / args.steps},
+        "gt_recovered_frac": r["ok_frac"],
+        "clocks": r["clocks"], "gpu_launches": r["launches"],
+        "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

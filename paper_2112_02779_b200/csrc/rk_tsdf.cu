@@ -1,0 +1,701 @@
+// rk_tsdf.cu -- K4 block activation over a GPU open-addressing hash, K5
+// voxel-parallel projective TSDF integration, block I/O and trilinear queries.
+//
+// Storage: a pool of 16^3 blocks, each 4096 float2
+// {tsdf, weight} voxels in C order (z fastest) = 32 KB, addressed by slot.
+// Keys are packed exactly like sdf_volume.py:64-71 (bias 2^17, 2^18 per axis)
+// into a 64-bit word; the hash maps key -> slot with linear probing.  Each
+// activation appends the frame's touched hash entries to a list (deduplicated
+// by a per-entry frame stamp) -- the touched set the reference returns.
+#include "rk_common.cuh"
+
+using namespace rk;
+
+static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+namespace {
+
+constexpr int kEdge = 16;
+constexpr int kVox = kEdge * kEdge * kEdge;
+constexpr long long kBias = 1ll << 17;
+constexpr long long kShift = 1ll << 18;
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr int kChunkBlocks = 600000 / kVox;  // sdf_volume.py:142 (146 blocks)
+
+struct Counters {
+  unsigned long long max_touched_key;  // largest packed key touched this frame
+  long long n_blocks;                  // allocated slots
+  long long updated;                   // voxels updated by the last integrate
+  int n_touched;
+  int n_fresh;
+  int overflow;
+  int n_points;                        // activation input size (gemv quirk)
+};
+
+__host__ __device__ __forceinline__ unsigned long long pack_key(long long x, long long y, long long z) {
+  return (unsigned long long)(((x + kBias) * kShift + (y + kBias)) * kShift + (z + kBias));
+}
+__host__ __device__ __forceinline__ void unpack_key(unsigned long long p, int& x, int& y, int& z) {
+  long long q = (long long)p;
+  z = (int)(q % kShift - kBias);
+  q /= kShift;
+  y = (int)(q % kShift - kBias);
+  x = (int)(q / kShift - kBias);
+}
+__device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+struct GridDev {
+  float2* vox;
+  int4* block_keys;
+  unsigned long long* h_keys;
+  int32_t* h_slot;
+  int32_t* h_stamp;
+  int32_t* touched;
+  int32_t* fresh;
+  Counters* ctr;
+  long long cap_blocks;
+  unsigned long long hash_mask;
+};
+
+// find or insert; returns hash position or -1 when the probe budget is spent
+__device__ long long hash_acquire(const GridDev& g, unsigned long long key, bool& inserted) {
+  unsigned long long h = mix64(key) & g.hash_mask;
+  inserted = false;
+  for (int probe = 0; probe < 4096; ++probe) {
+    unsigned long long k = *((volatile unsigned long long*)(g.h_keys + h));
+    if (k == key) return (long long)h;
+    if (k == kEmpty) {
+      unsigned long long prev = atomicCAS(g.h_keys + h, kEmpty, key);
+      if (prev == kEmpty) { inserted = true; return (long long)h; }
+      if (prev == key) return (long long)h;
+    }
+    h = (h + 1) & g.hash_mask;
+  }
+  return -1;
+}
+
+__device__ long long hash_find(const GridDev& g, unsigned long long key) {
+  unsigned long long h = mix64(key) & g.hash_mask;
+  for (int probe = 0; probe < 4096; ++probe) {
+    unsigned long long k = g.h_keys[h];
+    if (k == key) return (long long)h;
+    if (k == kEmpty) return -1;
+    h = (h + 1) & g.hash_mask;
+  }
+  return -1;
+}
+
+// one touched key: insert, dedupe per frame, remember fresh keys
+__device__ __forceinline__ void touch_key(const GridDev& g, int frame, long long x, long long y, long long z) {
+  unsigned long long key = pack_key(x, y, z);
+  bool inserted;
+  long long h = hash_acquire(g, key, inserted);
+  if (h < 0) { atomicExch(&g.ctr->overflow, 1); return; }
+  if (inserted) g.fresh[atomicAdd(&g.ctr->n_fresh, 1)] = (int32_t)h;
+  if (g.h_stamp[h] != frame && atomicExch(g.h_stamp + h, frame) != frame) {
+    g.touched[atomicAdd(&g.ctr->n_touched, 1)] = (int32_t)h;
+    atomicMax(&g.ctr->max_touched_key, key);
+  }
+}
+
+// all keys of blocks meeting the cube [p - radius, p + radius] (sdf_volume.py:88-106)
+__device__ __forceinline__ void touch_point(const GridDev& g, int frame, const double p[3],
+                                            double radius, double ext) {
+  long long lo[3], hi[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = (long long)floor(__ddiv_rn(__dsub_rn(p[c], radius), ext));
+    hi[c] = (long long)floor(__ddiv_rn(__dadd_rn(p[c], radius), ext));
+  }
+  for (long long x = lo[0]; x <= hi[0]; ++x)
+    for (long long y = lo[1]; y <= hi[1]; ++y)
+      for (long long z = lo[2]; z <= hi[2]; ++z) touch_key(g, frame, x, y, z);
+}
+
+__global__ void k_reset_frame(Counters* c) {
+  c->n_touched = 0;
+  c->n_fresh = 0;
+  c->max_touched_key = 0ull;
+  c->n_points = 0;
+}
+
+__global__ void k_activate_points(GridDev g, int frame, const double* __restrict__ pts, int64_t n,
+                                  double radius, double ext) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+  touch_point(g, frame, p, radius, ext);
+}
+
+__global__ void k_count_valid(const float* __restrict__ range, int n, float cmin, float cmax,
+                              Counters* c) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int ok = (i < n) && range_ok(range[i], cmin, cmax);
+  ok = __reduce_add_sync(0xffffffffu, ok);
+  if ((threadIdx.x & 31) == 0 && ok) atomicAdd(&c->n_points, ok);
+}
+
+// to_point_cloud -> pose.apply -> activate_blocks, fused (sdf_volume.py:198-208)
+__global__ void k_activate_image(GridDev g, SensorDev s, int frame, const float* __restrict__ range,
+                                 const double* __restrict__ pose12, double radius, double ext,
+                                 float cmin, float cmax) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.H * s.W) return;
+  float r = range[i];
+  if (!range_ok(r, cmin, cmax)) return;
+  double pose[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) pose[k] = pose12[k];
+  double p[3], w[3];
+  unproject_px(s, i / s.W, i % s.W, r, p);
+  xform_rows(pose, pose + 9, p[0], p[1], p[2], w, g.ctr->n_points == 1);
+  touch_point(g, frame, w, radius, ext);
+}
+
+// fresh keys -> pool slots (deterministic per key; slot order follows the list)
+__global__ void k_assign_slots(GridDev g) {
+  const int nf = g.ctr->n_fresh;
+  const long long base = g.ctr->n_blocks;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    int h = g.fresh[i];
+    long long slot = base + i;
+    if (slot < g.cap_blocks) {
+      g.h_slot[h] = (int32_t)slot;
+      int x, y, z;
+      unpack_key(g.h_keys[h], x, y, z);
+      g.block_keys[slot] = make_int4(x, y, z, 0);
+    } else {
+      g.h_slot[h] = -1;
+      atomicExch(&g.ctr->overflow, 1);
+    }
+  }
+}
+
+__global__ void k_finish_slots(GridDev g) {
+  long long nb = g.ctr->n_blocks + g.ctr->n_fresh;
+  g.ctr->n_blocks = nb < g.cap_blocks ? nb : g.cap_blocks;
+  g.ctr->n_fresh = 0;
+}
+
+// rotated voxel-centre lattice of one block, float32 (sdf_volume.py:160)
+__global__ void k_offsets(const double* __restrict__ inv12, double voxel, float* off) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kVox) return;
+  double R[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = inv12[k];
+  double l0 = __dmul_rn(__dadd_rn((double)(i >> 8), 0.5), voxel);
+  double l1 = __dmul_rn(__dadd_rn((double)((i >> 4) & 15), 0.5), voxel);
+  double l2 = __dmul_rn(__dadd_rn((double)(i & 15), 0.5), voxel);
+  double o[3];
+  xform_rows(R, nullptr, l0, l1, l2, o);
+  off[3 * i] = (float)o[0];
+  off[3 * i + 1] = (float)o[1];
+  off[3 * i + 2] = (float)o[2];
+}
+
+struct IntegrateArgs {
+  GridDev g;
+  SensorDev s;
+  const float* range;
+  const double* inv12;
+  const float* offsets;
+  double block_ext;  // 16 * voxel_size
+  float tau, max_w, cmin, cmax;
+  int free_space;
+  long long* updated;
+};
+
+// K5: persistent CTAs walk the touched list; each block's 4096 voxels are
+// projected into the (L2-resident) range image and folded into the running
+// average; voxels whose observation is rejected cost no state traffic.
+template <int MATH, int NT>
+__global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
+  extern __shared__ float sh_off[];  // kVox*3 rotated lattice (48 KB, dynamic)
+  __shared__ int sh_cnt[NT / 32];
+  for (int i = threadIdx.x; i < kVox * 3; i += NT) sh_off[i] = A.offsets[i];
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = A.inv12[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = A.inv12[9 + k];
+  __syncthreads();
+  const SensorDev& s = A.s;
+  const int n_touched = A.g.ctr->n_touched;
+  const unsigned long long max_key = A.g.ctr->max_touched_key;
+  // the reference integrates sorted keys in chunks of 146 blocks; a chunk of a
+  // single block goes through dgemv, which orders the FMA chain differently
+  const bool lone_tail = (n_touched % kChunkBlocks) == 1;
+  int count = 0;
+  for (int e = blockIdx.x; e < n_touched; e += gridDim.x) {
+    const int h = A.g.touched[e];
+    const int slot = A.g.h_slot[h];
+    if (slot < 0) continue;
+    const unsigned long long key = A.g.h_keys[h];
+    int kx, ky, kz;
+    unpack_key(key, kx, ky, kz);
+    double base[3];
+    xform_rows(R, t, __dmul_rn((double)kx, A.block_ext), __dmul_rn((double)ky, A.block_ext),
+               __dmul_rn((double)kz, A.block_ext), base, lone_tail && key == max_key);
+    const float bx = (float)base[0], by = (float)base[1], bz = (float)base[2];
+    float2* vox = A.g.vox + (size_t)slot * kVox;
+#pragma unroll 2
+    for (int i = threadIdx.x; i < kVox; i += NT) {
+      const float x = __fadd_rn(bx, sh_off[3 * i]);
+      const float y = __fadd_rn(by, sh_off[3 * i + 1]);
+      const float z = __fadd_rn(bz, sh_off[3 * i + 2]);
+      Proj32 p = project_f32<MATH>(s, x, y, z);
+      int col = (int)__fadd_rn(p.u, 0.5f);
+      if (col == s.W) col = 0;
+      const float px = __ldg(A.range + p.v * s.W + col);
+      bool ok = p.status == PROJ_OK && px > 0.0f && px >= A.cmin && px <= A.cmax && p.r <= A.cmax;
+      float d = __fsub_rn(px, p.r);
+      ok = ok && d >= -A.tau;
+      if (!A.free_space) ok = ok && d <= A.tau;
+      d = fminf(d, A.tau);
+      if (ok) {
+        float2 st = vox[i];
+        const float wn = __fadd_rn(st.y, 1.0f);
+        st.x = __fdiv_rn(__fadd_rn(__fmul_rn(st.y, st.x), d), wn);
+        st.y = fminf(wn, A.max_w);
+        vox[i] = st;
+        ++count;
+      }
+    }
+  }
+  count = __reduce_add_sync(0xffffffffu, count);
+  if ((threadIdx.x & 31) == 0) sh_cnt[threadIdx.x >> 5] = count;
+  __syncthreads();
+  if (threadIdx.x == 0 && A.updated) {
+    long long tot = 0;
+    for (int w = 0; w < NT / 32; ++w) tot += sh_cnt[w];
+    if (tot) atomicAdd((unsigned long long*)A.updated, (unsigned long long)tot);
+  }
+}
+
+__global__ void k_set_touched(GridDev g, int frame, const int32_t* __restrict__ keys, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // explicit frame_keys: they need not exist yet (integrate() on unknown keys
+  // raises KeyError in the reference; here they are simply skipped)
+  unsigned long long key = pack_key(keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
+  long long h = hash_find(g, key);
+  if (h < 0) return;
+  if (atomicExch(g.h_stamp + h, frame) != frame) {
+    g.touched[atomicAdd(&g.ctr->n_touched, 1)] = (int32_t)h;
+    atomicMax(&g.ctr->max_touched_key, key);
+  }
+}
+
+__global__ void k_keys_all(GridDev g, int32_t* out, long long cap) {
+  long long nb = g.ctr->n_blocks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nb && i < cap;
+       i += (long long)gridDim.x * blockDim.x) {
+    int4 k = g.block_keys[i];
+    out[3 * i] = k.x;
+    out[3 * i + 1] = k.y;
+    out[3 * i + 2] = k.z;
+  }
+}
+
+__global__ void k_keys_touched(GridDev g, int32_t* out, long long cap) {
+  int nt = g.ctr->n_touched;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nt && i < cap;
+       i += (long long)gridDim.x * blockDim.x) {
+    int x, y, z;
+    unpack_key(g.h_keys[g.touched[i]], x, y, z);
+    out[3 * i] = x;
+    out[3 * i + 1] = y;
+    out[3 * i + 2] = z;
+  }
+}
+
+__global__ void k_read_blocks(GridDev g, const int32_t* __restrict__ keys, int64_t n, float2* out,
+                              uint8_t* found) {
+  int64_t b = blockIdx.x;
+  if (b >= n) return;
+  long long h = hash_find(g, pack_key(keys[3 * b], keys[3 * b + 1], keys[3 * b + 2]));
+  int slot = h >= 0 ? g.h_slot[h] : -1;
+  if (threadIdx.x == 0 && found) found[b] = slot >= 0;
+  float2* dst = out + b * kVox;
+  if (slot < 0) {
+    for (int i = threadIdx.x; i < kVox; i += blockDim.x) dst[i] = make_float2(0.f, 0.f);
+    return;
+  }
+  const float2* src = g.vox + (size_t)slot * kVox;
+  for (int i = threadIdx.x; i < kVox; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void k_insert_keys(GridDev g, const int32_t* __restrict__ keys, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool inserted;
+  long long h = hash_acquire(g, pack_key(keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]), inserted);
+  if (h < 0) { atomicExch(&g.ctr->overflow, 1); return; }
+  if (inserted) g.fresh[atomicAdd(&g.ctr->n_fresh, 1)] = (int32_t)h;
+}
+
+__global__ void k_write_blocks(GridDev g, const int32_t* __restrict__ keys, int64_t n, const float2* src) {
+  int64_t b = blockIdx.x;
+  if (b >= n) return;
+  long long h = hash_find(g, pack_key(keys[3 * b], keys[3 * b + 1], keys[3 * b + 2]));
+  int slot = h >= 0 ? g.h_slot[h] : -1;
+  if (slot < 0) return;
+  float2* dst = g.vox + (size_t)slot * kVox;
+  for (int i = threadIdx.x; i < kVox; i += blockDim.x) dst[i] = src[b * kVox + i];
+}
+
+__device__ __forceinline__ void voxel_at(const GridDev& g, long long gx, long long gy, long long gz,
+                                         float& d, float& w, bool& found) {
+  long long bx = gx >= 0 ? gx / kEdge : -((-gx + kEdge - 1) / kEdge);
+  long long by = gy >= 0 ? gy / kEdge : -((-gy + kEdge - 1) / kEdge);
+  long long bz = gz >= 0 ? gz / kEdge : -((-gz + kEdge - 1) / kEdge);
+  long long h = hash_find(g, pack_key(bx, by, bz));
+  int slot = h >= 0 ? g.h_slot[h] : -1;
+  found = slot >= 0;
+  d = w = 0.f;
+  if (!found) return;
+  int lx = (int)(gx - bx * kEdge), ly = (int)(gy - by * kEdge), lz = (int)(gz - bz * kEdge);
+  float2 v = g.vox[(size_t)slot * kVox + (lx * kEdge + ly) * kEdge + lz];
+  d = v.x;
+  w = v.y;
+}
+
+// query_sdf_many (sdf_volume.py:221-244): trilinear over the 8 enclosing centres
+__global__ void k_query(GridDev g, double voxel, const double* __restrict__ pts, int64_t n,
+                        double* sdf, double* wt, uint8_t* obs) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double gq[3], fr[3];
+  long long b[3];
+  for (int c = 0; c < 3; ++c) {
+    gq[c] = __dsub_rn(__ddiv_rn(pts[3 * i + c], voxel), 0.5);
+    double f = floor(gq[c]);
+    b[c] = (long long)f;
+    fr[c] = __dsub_rn(gq[c], (double)b[c]);
+  }
+  double s_acc = 0.0, w_acc = 0.0;
+  bool ok = true;
+  for (int corner = 0; corner < 8; ++corner) {
+    int cx = (corner >> 2) & 1, cy = (corner >> 1) & 1, cz = corner & 1;
+    double w0 = cx ? fr[0] : __dsub_rn(1.0, fr[0]);
+    double w1 = cy ? fr[1] : __dsub_rn(1.0, fr[1]);
+    double w2 = cz ? fr[2] : __dsub_rn(1.0, fr[2]);
+    double cw = __dmul_rn(__dmul_rn(w0, w1), w2);
+    float d, w;
+    bool found;
+    voxel_at(g, b[0] + cx, b[1] + cy, b[2] + cz, d, w, found);
+    ok = ok && found && w > 0.f;
+    s_acc = __dadd_rn(s_acc, __dmul_rn(cw, (double)d));
+    w_acc = __dadd_rn(w_acc, __dmul_rn(cw, (double)w));
+  }
+  sdf[i] = s_acc;
+  wt[i] = w_acc;
+  obs[i] = ok ? 1 : 0;
+}
+
+__global__ void k_rehash(GridDev g, long long nb) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nb;
+       i += (long long)gridDim.x * blockDim.x) {
+    int4 k = g.block_keys[i];
+    bool inserted;
+    long long h = hash_acquire(g, pack_key(k.x, k.y, k.z), inserted);
+    if (h >= 0) g.h_slot[h] = (int32_t)i;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+struct rk_grid {
+  double voxel, trunc;
+  float max_weight;
+  int free_space;
+  int frame;
+  GridDev d;
+  unsigned long long hash_cap;
+  float* offsets;  // 4096*3
+};
+
+static unsigned long long pow2_at_least(unsigned long long x) {
+  unsigned long long p = 1024;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+static int alloc_tables(rk_grid* g, long long cap_blocks, cudaStream_t st) {
+  GridDev& d = g->d;
+  unsigned long long hcap = pow2_at_least((unsigned long long)cap_blocks * 4ull);
+  RK_CUDA(cudaMalloc(&d.vox, (size_t)cap_blocks * kVox * sizeof(float2)));
+  RK_CUDA(cudaMemsetAsync(d.vox, 0, (size_t)cap_blocks * kVox * sizeof(float2), st));
+  RK_CUDA(cudaMalloc(&d.block_keys, (size_t)cap_blocks * sizeof(int4)));
+  RK_CUDA(cudaMalloc(&d.h_keys, hcap * sizeof(unsigned long long)));
+  RK_CUDA(cudaMemsetAsync(d.h_keys, 0xff, hcap * sizeof(unsigned long long), st));
+  RK_CUDA(cudaMalloc(&d.h_slot, hcap * sizeof(int32_t)));
+  RK_CUDA(cudaMemsetAsync(d.h_slot, 0xff, hcap * sizeof(int32_t), st));
+  RK_CUDA(cudaMalloc(&d.h_stamp, hcap * sizeof(int32_t)));
+  RK_CUDA(cudaMemsetAsync(d.h_stamp, 0, hcap * sizeof(int32_t), st));
+  RK_CUDA(cudaMalloc(&d.touched, hcap * sizeof(int32_t)));
+  RK_CUDA(cudaMalloc(&d.fresh, hcap * sizeof(int32_t)));
+  d.cap_blocks = cap_blocks;
+  d.hash_mask = hcap - 1;
+  g->hash_cap = hcap;
+  return RK_OK;
+}
+
+static void free_tables(GridDev& d) {
+  cudaFree(d.vox);
+  cudaFree(d.block_keys);
+  cudaFree(d.h_keys);
+  cudaFree(d.h_slot);
+  cudaFree(d.h_stamp);
+  cudaFree(d.touched);
+  cudaFree(d.fresh);
+}
+
+extern "C" int rk_grid_create(double voxel_size, double truncation, float max_weight,
+                              int32_t free_space, int64_t capacity_blocks, rk_grid** out) {
+  if (!(voxel_size > 0) || !(truncation > 0)) {
+    rk_set_error("voxel size and truncation must be > 0");
+    return RK_EGENERIC;
+  }
+  rk_grid* g = new rk_grid();
+  g->voxel = voxel_size;
+  g->trunc = truncation;
+  g->max_weight = max_weight;
+  g->free_space = free_space;
+  g->frame = 1;
+  if (capacity_blocks < 64) capacity_blocks = 64;
+  int rc = alloc_tables(g, capacity_blocks, 0);
+  if (rc) { delete g; return rc; }
+  RK_CUDA(cudaMalloc(&g->d.ctr, sizeof(Counters)));
+  RK_CUDA(cudaMemset(g->d.ctr, 0, sizeof(Counters)));
+  RK_CUDA(cudaMalloc(&g->offsets, kVox * 3 * sizeof(float)));
+  RK_CUDA(cudaDeviceSynchronize());
+  *out = g;
+  return RK_OK;
+}
+
+extern "C" int rk_grid_destroy(rk_grid* g) {
+  if (!g) return RK_OK;
+  cudaDeviceSynchronize();
+  free_tables(g->d);
+  cudaFree(g->d.ctr);
+  cudaFree(g->offsets);
+  delete g;
+  return RK_OK;
+}
+
+extern "C" int rk_grid_reserve(rk_grid* g, int64_t capacity_blocks, void* stream) {
+  cudaStream_t st = S(stream);
+  if (capacity_blocks <= g->d.cap_blocks) return RK_OK;
+  Counters c;
+  RK_CUDA(cudaMemcpyAsync(&c, g->d.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+  RK_CUDA(cudaStreamSynchronize(st));
+  GridDev old = g->d;
+  int rc = alloc_tables(g, capacity_blocks, st);
+  if (rc) return rc;
+  long long nb = c.n_blocks;
+  if (nb > 0) {
+    RK_CUDA(cudaMemcpyAsync(g->d.vox, old.vox, (size_t)nb * kVox * sizeof(float2),
+                            cudaMemcpyDeviceToDevice, st));
+    RK_CUDA(cudaMemcpyAsync(g->d.block_keys, old.block_keys, (size_t)nb * sizeof(int4),
+                            cudaMemcpyDeviceToDevice, st));
+    k_rehash<<<256, 256, 0, st>>>(g->d, nb);
+    RK_LAUNCHED("k_rehash");
+  }
+  c.overflow = 0;
+  c.n_touched = 0;
+  c.n_fresh = 0;
+  RK_CUDA(cudaMemcpyAsync(g->d.ctr, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+  RK_CUDA(cudaStreamSynchronize(st));
+  free_tables(old);
+  g->frame += 1;
+  return RK_OK;
+}
+
+extern "C" int rk_grid_info(rk_grid* g, int64_t* out4, void* stream) {
+  cudaStream_t st = S(stream);
+  Counters c;
+  RK_CUDA(cudaMemcpyAsync(&c, g->d.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+  RK_CUDA(cudaStreamSynchronize(st));
+  out4[0] = c.n_blocks;
+  out4[1] = g->d.cap_blocks;
+  out4[2] = c.overflow;
+  out4[3] = c.n_touched;
+  return RK_OK;
+}
+
+static int finish_activation(rk_grid* g, cudaStream_t st) {
+  k_assign_slots<<<64, 256, 0, st>>>(g->d);
+  k_finish_slots<<<1, 1, 0, st>>>(g->d);
+  RK_LAUNCHED("rk_grid activation");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_activate_points(rk_grid* g, const double* pts, int64_t n, double radius,
+                                       void* stream) {
+  cudaStream_t st = S(stream);
+  g->frame += 1;
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  if (n > 0)
+    k_activate_points<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, g->frame, pts, n, radius,
+                                                                    kEdge * g->voxel);
+  return finish_activation(g, st);
+}
+
+extern "C" int rk_grid_activate_image(rk_grid* g, const rk_sensor* s, const float* range,
+                                      const double* pose12, double radius, float clip_min,
+                                      float clip_max, void* stream) {
+  cudaStream_t st = S(stream);
+  g->frame += 1;
+  const int n = s->dev.H * s->dev.W;
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  k_count_valid<<<(n + 255) / 256, 256, 0, st>>>(range, n, clip_min, clip_max, g->d.ctr);
+  k_activate_image<<<(n + 255) / 256, 256, 0, st>>>(g->d, s->dev, g->frame, range, pose12, radius,
+                                                    kEdge * g->voxel, clip_min, clip_max);
+  return finish_activation(g, st);
+}
+
+extern "C" int rk_grid_set_touched(rk_grid* g, const int32_t* keys, int64_t n, void* stream) {
+  cudaStream_t st = S(stream);
+  g->frame += 1;
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  if (n > 0) k_set_touched<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, g->frame, keys, n);
+  RK_LAUNCHED("k_set_touched");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* range,
+                                 const double* inv12, float clip_min, float clip_max, int math,
+                                 int64_t* updated, void* stream) {
+  cudaStream_t st = S(stream);
+  k_offsets<<<kVox / 256, 256, 0, st>>>(inv12, g->voxel, g->offsets);
+  IntegrateArgs a;
+  a.g = g->d;
+  a.s = s->dev;
+  a.range = range;
+  a.inv12 = inv12;
+  a.offsets = g->offsets;
+  a.block_ext = kEdge * g->voxel;
+  a.tau = (float)g->trunc;
+  a.max_w = g->max_weight;
+  a.cmin = clip_min;
+  a.cmax = clip_max;
+  a.free_space = g->free_space;
+  a.updated = reinterpret_cast<long long*>(updated);
+  constexpr int NT = 256;
+  const unsigned grid = 148 * 4;
+  const size_t smem = kVox * 3 * sizeof(float);
+  static bool attr_set = false;
+  if (!attr_set) {
+    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_CR, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_FAST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  if (math == MATH_CR)
+    k_integrate<MATH_CR, NT><<<grid, NT, smem, st>>>(a);
+  else
+    k_integrate<MATH_FAST, NT><<<grid, NT, smem, st>>>(a);
+  RK_LAUNCHED("k_integrate");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_keys(rk_grid* g, int touched_only, int32_t* keys_out, int64_t cap,
+                            int64_t* n_host, void* stream) {
+  cudaStream_t st = S(stream);
+  Counters c;
+  RK_CUDA(cudaMemcpyAsync(&c, g->d.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+  RK_CUDA(cudaStreamSynchronize(st));
+  long long n = touched_only ? c.n_touched : c.n_blocks;
+  if (n_host) *n_host = n;
+  if (keys_out && cap > 0 && n > 0) {
+    if (touched_only) k_keys_touched<<<128, 256, 0, st>>>(g->d, keys_out, cap);
+    else k_keys_all<<<128, 256, 0, st>>>(g->d, keys_out, cap);
+    RK_LAUNCHED("rk_grid_keys");
+  }
+  return RK_OK;
+}
+
+extern "C" int rk_grid_read_blocks(rk_grid* g, const int32_t* keys, int64_t n, float* vox,
+                                   uint8_t* found, void* stream) {
+  if (n <= 0) return RK_OK;
+  k_read_blocks<<<(unsigned)n, 256, 0, S(stream)>>>(g->d, keys, n, reinterpret_cast<float2*>(vox), found);
+  RK_LAUNCHED("k_read_blocks");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_write_blocks(rk_grid* g, const int32_t* keys, int64_t n, const float* vox,
+                                    void* stream) {
+  cudaStream_t st = S(stream);
+  if (n <= 0) return RK_OK;
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  k_insert_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, keys, n);
+  int rc = finish_activation(g, st);
+  if (rc) return rc;
+  k_write_blocks<<<(unsigned)n, 256, 0, st>>>(g->d, keys, n, reinterpret_cast<const float2*>(vox));
+  RK_LAUNCHED("k_write_blocks");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_query(rk_grid* g, const double* pts, int64_t n, double* sdf, double* weight,
+                             uint8_t* observed, void* stream) {
+  if (n <= 0) return RK_OK;
+  k_query<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(g->d, g->voxel, pts, n, sdf, weight,
+                                                               observed);
+  RK_LAUNCHED("k_query");
+  return RK_OK;
+}
+
+int rk_grid_view_(rk_grid* g, GridView* v) {
+  Counters c;
+  RK_CUDA(cudaMemcpy(&c, g->d.ctr, sizeof(c), cudaMemcpyDeviceToHost));
+  v->vox = g->d.vox;
+  v->block_keys = g->d.block_keys;
+  v->h_keys = g->d.h_keys;
+  v->h_slot = g->d.h_slot;
+  v->hash_mask = g->d.hash_mask;
+  v->n_blocks = c.n_blocks;
+  return RK_OK;
+}
+
+double rk_grid_voxel_(rk_grid* g) { return g->voxel; }
+
+namespace {
+__global__ void k_clear_blocks(GridDev g) {
+  const long long nb = g.ctr->n_blocks;
+  float4* v = reinterpret_cast<float4*>(g.vox);
+  const long long n4 = nb * (kVox / 2);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__global__ void k_clear_counters(Counters* c) {
+  c->n_blocks = 0;
+  c->n_touched = 0;
+  c->n_fresh = 0;
+  c->overflow = 0;
+  c->max_touched_key = 0ull;
+  c->updated = 0;
+  c->n_points = 0;
+}
+}  // namespace
+
+// empty the grid without freeing it (async; keeps capacity)
+extern "C" int rk_grid_clear(rk_grid* g, void* stream) {
+  cudaStream_t st = S(stream);
+  k_clear_blocks<<<148 * 8, 256, 0, st>>>(g->d);
+  RK_CUDA(cudaMemsetAsync(g->d.h_keys, 0xff, g->hash_cap * sizeof(unsigned long long), st));
+  RK_CUDA(cudaMemsetAsync(g->d.h_slot, 0xff, g->hash_cap * sizeof(int32_t), st));
+  k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr);
+  RK_LAUNCHED("rk_grid_clear");
+  g->frame += 1;
+  return RK_OK;
+}

@@ -1,0 +1,122 @@
+"""Batched device pipelines behind the drop-in API: the callers the reference's
+CLI runs in Python loops (cli.py:248-328 odometry / eval-reg pair sweeps,
+cli.py:267-283 integrate) expressed as a few launches over device buffers.
+
+* ``render_batch``   -- synthetic inputs on the device (synth.py:108-134, N4)
+* ``integrate_sequence`` -- activate + integrate F posed frames into one grid
+  with no host synchronisation between frames
+* ``shard`` / ``gather_poses`` -- one-process-per-GPU partitioning of
+  independent pairs: contiguous slices, no data-path collective
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from . import lidar_model as lm
+from .sdf_volume import VoxelBlockGrid
+from .se3 import RigidTransform
+
+_KIND = {"plane": 0, "sphere": 1, "box": 2}
+
+
+def encode_scene(prims) -> np.ndarray:
+    """Scene tuples (see scenes.py) -> (n, 16) float64 rows for rk_render."""
+    rows = np.zeros((len(prims), 16))
+    for i, p in enumerate(prims):
+        rows[i, 0] = _KIND[p[0]]
+        if p[0] == "plane":
+            rows[i, 1:4] = p[1]
+            rows[i, 4] = p[2]
+        elif p[0] == "sphere":
+            rows[i, 1:4] = p[1]
+            rows[i, 4] = p[2]
+        else:
+            rows[i, 1:4] = p[1]
+            rows[i, 4:7] = p[2]
+            R = np.eye(3) if len(p) < 4 or p[3] is None else np.asarray(p[3], float)
+            rows[i, 7:16] = R.reshape(-1)
+    return rows
+
+
+def poses_to_rows(poses) -> np.ndarray:
+    return np.stack([p.as_row12() for p in poses]) if poses else np.zeros((0, 12))
+
+
+def render_batch(intr: lm.LidarIntrinsics, scene, poses):
+    """(B, H, W) float32 device range images of ``scene`` seen from each
+    world-from-sensor pose."""
+    prims = nat.to_dev(encode_scene(scene), np.float64)
+    P = nat.to_dev(poses_to_rows(poses), np.float64)
+    B = len(poses)
+    out = nat.empty((B, intr.height, intr.width), np.float32)
+    if B:
+        nat.call("rk_render", lm.device_sensor(intr), nat.ptr(prims), prims.shape[0], nat.ptr(P), B,
+                 nat.ptr(out), nat.stream_ptr())
+    return out
+
+
+def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, poses_w,
+                       inv_w=None, clip_min: float = 0.0, clip_max: float = np.inf,
+                       radius: float | None = None, updated=None):
+    """integrate_cloud_frame over F device frames, fully asynchronous.
+
+    frames: (F, H, W) float32 device tensor; poses_w: (F, 12) float64 device
+    world-from-frame rows; inv_w: (F, 12) their inverses formed on the host
+    with numpy (as the reference's integrate() does) -- computed if None.
+    Returns the device int64 counter of updated voxels.  The caller must size
+    the grid (``grid.reserve``) and may check ``grid.info()`` for overflow.
+    """
+    h = grid._prepare()
+    sensor = lm.device_sensor(intr)
+    radius = grid.truncation if radius is None else radius
+    if inv_w is None:
+        host = nat.to_host(poses_w)
+        inv_w = nat.to_dev(np.stack([RigidTransform(r[:9].reshape(3, 3), r[9:]).inverse().as_row12()
+                                     for r in host]), np.float64)
+    if updated is None:
+        updated = nat.zeros((1,), np.int64)
+    st = nat.stream_ptr()
+    cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
+    math = lm.default_math()
+    for f in range(frames.shape[0]):
+        nat.call("rk_grid_activate_image", h, sensor, nat.ptr(frames[f]), nat.ptr(poses_w[f]),
+                 float(radius), cmin, cmax, st)
+        nat.call("rk_grid_integrate", h, sensor, nat.ptr(frames[f]), nat.ptr(inv_w[f]), cmin, cmax,
+                 math, nat.ptr(updated), st)
+    grid.blocks._bump()
+    return updated
+
+
+# launches issued per call (the bench's gpu_launches accounting)
+LAUNCHES_PER_FRAME = 7     # reset, count, activate, assign, finish, offsets, integrate
+LAUNCHES_CLEAR = 2         # k_clear_blocks, k_clear_counters (+2 memsets)
+
+
+def clear_grid(grid: VoxelBlockGrid):
+    nat.call("rk_grid_clear", grid._prepare(), nat.stream_ptr())
+    grid.blocks._bump()
+
+
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) slice of n independent units for one rank."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def gather_poses(local_poses, n_total: int, rank: int, world: int):
+    """All-gather per-rank (n_i, 12) pose slices into (n_total, 12) on every
+    rank (torch.distributed; the only cross-rank traffic of the ICP batch)."""
+    t = nat.torch()
+    import torch.distributed as dist
+    if world == 1:
+        return local_poses
+    sizes = [shard(n_total, r, world) for r in range(world)]
+    width = max(hi - lo for lo, hi in sizes)
+    pad = t.zeros((width, local_poses.shape[1]), dtype=local_poses.dtype, device=local_poses.device)
+    pad[:local_poses.shape[0]] = local_poses
+    bufs = [t.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    return t.cat([b[:hi - lo] for b, (lo, hi) in zip(bufs, sizes)])

@@ -1,0 +1,318 @@
+"""Projective point-to-plane registration -- drop-in for rangekit/registration.py.
+
+``register`` runs the whole coarse-to-fine schedule in one launch of the K3
+kernel (``rk_register_batch``): association, residual/Jacobian, IRLS weights,
+the 6x6 normal-equation reduction, the float64 solve, the twist update and the
+early-exit test all happen on the device.  ``register_batch`` exposes the same
+kernel over many independent pairs (the odometry / eval-reg callers of the
+reference, cli.py:248-328).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from . import lidar_model as lm
+from .errors import DegenerateGeometry, EmptyInput, MissingNormals
+from .range_image import NormalImage, RangeImage, compute_normal_map, normals_cross_batch
+from .se3 import RigidTransform
+
+DEFAULT_SCHEDULE = ((4, 20), (2, 20), (1, 10))
+SINGLE_SCALE_SCHEDULE = ((1, 50),)
+
+ICP_CONVERGED, ICP_TOO_FEW, ICP_DEGENERATE = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class RegistrationConfig:
+    """Same fields and validation as registration.py:29-57.  ``threads`` is
+    accepted for compatibility and ignored (the device reduction order is
+    fixed, so results are bitwise reproducible regardless)."""
+
+    kernel_scale: float = 0.5
+    max_correspondence_dist: float = 0.5
+    schedule: tuple[tuple[int, int], ...] = DEFAULT_SCHEDULE
+    rot_eps: float = 1e-4
+    trans_eps: float = 1e-4
+    clip_min: float = 0.0
+    clip_max: float = np.inf
+    normal_method: str = "cross"
+    min_correspondences: int = 6
+    scale_with_stride: bool = True
+    threads: int | None = None
+
+    def __post_init__(self):
+        strides = [s for s, _ in self.schedule]
+        if any(s < 1 for s in strides) or any(n < 1 for _, n in self.schedule):
+            raise ValueError("strides and iteration counts must be >= 1")
+        if list(strides) != sorted(strides, reverse=True):
+            raise ValueError("schedule strides must be non-increasing (coarse to fine)")
+        if self.kernel_scale <= 0:
+            raise ValueError("kernel scale must be > 0")
+        if len(self.schedule) > 8:
+            raise ValueError("at most 8 pyramid levels are supported")
+
+    def to_c(self, math: int | None = None) -> nat.IcpConfig:
+        c = nat.IcpConfig()
+        c.kernel_scale = float(self.kernel_scale)
+        c.max_dist = float(self.max_correspondence_dist)
+        c.rot_eps = float(self.rot_eps)
+        c.trans_eps = float(self.trans_eps)
+        c.clip_min = float(np.float32(self.clip_min))
+        c.clip_max = float(np.float32(self.clip_max))
+        c.n_levels = len(self.schedule)
+        for i, (s, n) in enumerate(self.schedule):
+            c.strides[i] = int(s)
+            c.iters[i] = int(n)
+        c.min_corr = int(self.min_correspondences)
+        c.scale_with_stride = int(bool(self.scale_with_stride))
+        c.math = lm.default_math() if math is None else int(math)
+        return c
+
+    @property
+    def max_iterations(self) -> int:
+        return int(sum(n for _, n in self.schedule))
+
+
+@dataclass
+class IterationStats:
+    stride: int
+    iteration: int
+    n_correspondences: int
+    cost: float
+    inlier_rmse: float
+
+
+@dataclass
+class RegistrationResult:
+    pose: RigidTransform
+    stats: list[IterationStats] = field(default_factory=list)
+    converged: bool = True
+
+    @property
+    def iterations(self) -> int:
+        return len(self.stats)
+
+
+@dataclass
+class CorrespondenceSet:
+    source: np.ndarray
+    target: np.ndarray
+    normal: np.ndarray
+
+    def __len__(self) -> int:
+        return self.source.shape[0]
+
+
+def _pose_dev(pose: RigidTransform):
+    return nat.to_dev(pose.as_row12(), np.float64)
+
+
+def initial_translation_by_centroids(src, dst) -> RigidTransform:
+    """Identity rotation, t = mean(dst) - mean(src) (registration.py:96-102),
+    reduced on the device in a fixed order."""
+    s = nat.to_dev(src, np.float64).reshape(-1, 3)
+    d = nat.to_dev(dst, np.float64).reshape(-1, 3)
+    if s.shape[0] == 0 or d.shape[0] == 0:
+        raise EmptyInput("centroid alignment needs non-empty point sets")
+    out = nat.empty((3,), np.float64)
+    work = nat.empty((6 * 64,), np.float64)
+    nat.call("rk_centroid_translation", nat.ptr(s), s.shape[0], nat.ptr(d), d.shape[0],
+             nat.ptr(out), nat.ptr(work), nat.stream_ptr())
+    return RigidTransform(t=nat.to_host(out))
+
+
+def robust_weight(residual, k: float):
+    """Scalar IRLS weight 1/sqrt(1 + (e/k)^2) (registration.py:105-108).
+    Host helper for tests/diagnostics; the kernels compute it inline."""
+    e = np.asarray(residual, dtype=float)
+    return 1.0 / np.sqrt(1.0 + (e / k) ** 2)
+
+
+def pseudo_huber(residual, k: float):
+    """rho(e) = k^2 (sqrt(1 + (e/k)^2) - 1) (registration.py:111-114); host helper."""
+    e = np.asarray(residual, dtype=float)
+    return k * k * (np.sqrt(1.0 + (e / k) ** 2) - 1.0)
+
+
+def projective_correspondences(src_points, dst_img: RangeImage, dst_normals: NormalImage,
+                               pose: RigidTransform, max_dist: float, stride: int = 1,
+                               single: bool = False) -> CorrespondenceSet:
+    """Project transformed source points into dst, read the stored range of the
+    nearest stride-aligned pixel, gate by distance (registration.py:117-187)."""
+    if dst_normals is None:
+        raise MissingNormals("destination normal map is required")
+    intr = dst_img.intrinsics
+    sensor = lm.device_sensor(intr)
+    src = nat.to_dev(src_points, np.float64).reshape(-1, 3)
+    n = src.shape[0]
+    surf = dst_normals.device_surfel(dst_img)
+    pose_d = _pose_dev(pose)
+    keep = nat.empty((n,), np.uint8)
+    st = nat.stream_ptr()
+    if single:
+        tgt = nat.empty((n, 3), np.float32)
+        nrm = nat.empty((n, 3), np.float32)
+        if n:
+            nat.call("rk_correspondences_f32", sensor, nat.ptr(src), n, None, nat.ptr(surf),
+                     nat.ptr(pose_d), float(max_dist), int(stride), lm.default_math(),
+                     nat.ptr(keep), nat.ptr(tgt), nat.ptr(nrm), st)
+    else:
+        moved = nat.empty((n, 3), np.float64)
+        tgt = nat.empty((n, 3), np.float64)
+        nrm = nat.empty((n, 3), np.float64)
+        if n:
+            nat.call("rk_transform_points", nat.ptr(pose_d), nat.ptr(src), n, nat.ptr(moved), st)
+            u, v, _, status = lm.project_many(moved, intr, single=False, refine=True)
+            nat.call("rk_associate_f64", sensor, nat.ptr(moved), nat.ptr(u), nat.ptr(v),
+                     nat.ptr(status), n, nat.ptr(surf), float(max_dist), int(stride),
+                     nat.ptr(keep), nat.ptr(tgt), nat.ptr(nrm), st)
+    idx = nat.empty((max(n, 1),), np.int32)
+    cnt = nat.zeros((1,), np.int32)
+    if n:
+        nat.call("rk_compact_mask", nat.ptr(keep), n, nat.ptr(idx), nat.ptr(cnt), st)
+    m = int(cnt.item())
+    sel = idx[:m].long()
+    out = CorrespondenceSet(src[sel], tgt[sel], nrm[sel])
+    if nat.is_tensor(src_points) and src_points.is_cuda:
+        return out
+    return CorrespondenceSet(nat.to_host(out.source), nat.to_host(out.target),
+                             nat.to_host(out.normal))
+
+
+def _corr_dev(corr: CorrespondenceSet):
+    return (nat.to_dev(corr.source, np.float64).reshape(-1, 3),
+            nat.to_dev(corr.target, np.float64).reshape(-1, 3),
+            nat.to_dev(corr.normal, np.float64).reshape(-1, 3))
+
+
+def point_to_plane_residuals(corr: CorrespondenceSet, pose: RigidTransform):
+    src, tgt, nrm = _corr_dev(corr)
+    n = src.shape[0]
+    out = nat.empty((n,), np.float64)
+    if n:
+        nat.call("rk_point_to_plane_residuals", nat.ptr(_pose_dev(pose)), nat.ptr(src),
+                 nat.ptr(tgt), nat.ptr(nrm), n, nat.ptr(out), nat.stream_ptr())
+    return nat.to_host(out)
+
+
+def _gauss_newton_solve(corr: CorrespondenceSet, pose: RigidTransform, kernel_scale: float):
+    """float64 robust GN step (registration.py:208-234): normal equations
+    reduced on the device, the 6x6 condition test and solve on the host."""
+    n = len(corr)
+    if n < 6:
+        raise DegenerateGeometry(f"need at least 6 correspondences, got {n}")
+    src, tgt, nrm = _corr_dev(corr)
+    out = nat.empty((29,), np.float64)
+    work = nat.empty((64 * 29,), np.float64)
+    nat.call("rk_normal_equations_f64", nat.ptr(_pose_dev(pose)), nat.ptr(src), nat.ptr(tgt),
+             nat.ptr(nrm), n, float(kernel_scale), nat.ptr(out), nat.ptr(work), nat.stream_ptr())
+    acc = nat.to_host(out)
+    H = np.zeros((6, 6))
+    iu = np.triu_indices(6)
+    H[iu] = acc[:21]
+    H = H + np.triu(H, 1).T
+    b = acc[21:27]
+    if np.linalg.cond(H) > 1e12:
+        raise DegenerateGeometry("normal equations are ill-conditioned (rank-deficient geometry)")
+    xi = np.linalg.solve(H, b)
+    cost = float(kernel_scale ** 2 * acc[27])
+    rmse = float(np.sqrt(acc[28] / n))
+    return xi, cost, rmse
+
+
+def gauss_newton_step(corr: CorrespondenceSet, pose: RigidTransform, kernel_scale: float):
+    xi, cost, _ = _gauss_newton_solve(corr, pose, kernel_scale)
+    return xi, cost
+
+
+# ------------------------------------------------------------------ batch API
+
+@dataclass
+class BatchResult:
+    """Device-resident results of ``register_batch``."""
+
+    poses: "object"        # (B, 12) float64 [R row-major, t]
+    status: "object"       # (B,) int32 ICP_*
+    iterations: "object"   # (B,) int32
+    stats: "object | None"  # (B, max_iters, 5) float64 or None
+
+    def pose(self, b: int) -> RigidTransform:
+        p = nat.to_host(self.poses[b])
+        return RigidTransform(p[:9].reshape(3, 3), p[9:])
+
+
+def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels=None,
+                   pair_src=None, pair_dst=None, inits=None,
+                   config: RegistrationConfig = RegistrationConfig(), with_stats: bool = False,
+                   math: int | None = None, pt_iters=None) -> BatchResult:
+    """register() for B independent pairs in one launch (device tensors in/out).
+
+    src_ranges / dst_ranges: (P, H, W) float32 CUDA tensors (image pools);
+    pair_src / pair_dst: (B,) int32 indices into them (default: arange);
+    dst_surfels: (P, H, W, 4) from ``normals_cross_batch`` (computed if None);
+    inits: (B, 12) float64 initial poses (default identity);
+    pt_iters: optional (1,) int64 device counter of executed point-iterations.
+    """
+    t = nat.torch()
+    src = src_ranges.contiguous()
+    dst = dst_ranges.contiguous()
+    if dst_surfels is None:
+        dst_surfels = normals_cross_batch(intr, dst)
+    B = src.shape[0] if pair_src is None else pair_src.shape[0]
+    dev = nat.device()
+    if pair_src is None:
+        pair_src = t.arange(B, dtype=t.int32, device=dev)
+    if pair_dst is None:
+        pair_dst = t.arange(B, dtype=t.int32, device=dev)
+    if inits is None:
+        inits = t.zeros((B, 12), dtype=t.float64, device=dev)
+        inits[:, 0] = inits[:, 4] = inits[:, 8] = 1.0
+    poses = t.empty((B, 12), dtype=t.float64, device=dev)
+    status = t.empty((B,), dtype=t.int32, device=dev)
+    iters = t.empty((B,), dtype=t.int32, device=dev)
+    max_it = config.max_iterations
+    stats = t.empty((B, max_it, 5), dtype=t.float64, device=dev) if with_stats else None
+    cfg = config.to_c(math)
+    nat.call("rk_register_batch", lm.device_sensor(intr), nat.ptr(src), nat.ptr(dst),
+             nat.ptr(dst_surfels), nat.ptr(pair_src.to(t.int32).contiguous()),
+             nat.ptr(pair_dst.to(t.int32).contiguous()), B, nat.ptr(inits.contiguous()),
+             C.byref(cfg), nat.ptr(poses), nat.ptr(status), nat.ptr(iters),
+             nat.ptr(stats), max_it if with_stats else 0, nat.ptr(pt_iters), nat.stream_ptr())
+    return BatchResult(poses, status, iters, stats)
+
+
+def register(src_img: RangeImage, dst_img: RangeImage, init: RigidTransform | None = None,
+             config: RegistrationConfig = RegistrationConfig(),
+             dst_normals: NormalImage | None = None) -> RegistrationResult:
+    """Align src to dst over the stride schedule (registration.py:237-289)."""
+    pose = RigidTransform.identity() if init is None else init
+    if dst_normals is None:
+        dst_normals = compute_normal_map(dst_img, method=config.normal_method)
+    intr = dst_img.intrinsics
+    t = nat.torch()
+    src = src_img.device_data().reshape(1, intr.height, intr.width)
+    dst = dst_img.device_data().reshape(1, intr.height, intr.width)
+    surf = dst_normals.device_surfel(dst_img).reshape(1, intr.height, intr.width, 4)
+    init_d = nat.to_dev(pose.as_row12()[None, :], np.float64)
+    res = register_batch(intr, src, dst, surf, inits=init_d, config=config, with_stats=True)
+    status = int(res.status[0].item())
+    n_it = int(res.iterations[0].item())
+    if status == ICP_DEGENERATE:
+        raise DegenerateGeometry("normal equations are ill-conditioned (rank-deficient geometry)")
+    rows = nat.to_host(res.stats[0, :n_it]) if n_it else np.zeros((0, 5))
+    stats = [IterationStats(int(r[0]), int(r[1]), int(r[2]), float(r[3]), float(r[4])) for r in rows]
+    del t
+    return RegistrationResult(pose=res.pose(0), stats=stats, converged=status == ICP_CONVERGED)
+
+
+def timed_register(*args, **kwargs):
+    """register() plus wall-clock milliseconds (registration.py:370-374)."""
+    t0 = time.perf_counter()
+    res = register(*args, **kwargs)
+    return res, (time.perf_counter() - t0) * 1e3

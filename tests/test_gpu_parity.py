@@ -1,0 +1,401 @@
+"""Parity of the CUDA path (librkb200.so, via the package API / C ABI) with the
+reference's golden vectors and with the CPU oracle.
+
+Contract (BASELINE.json north_star):
+* bit-exact: sensor tables, row lookup, pyramid indices and point clouds,
+  normals, voxel-block allocation; with RK_MATH_CR (float64-evaluated
+  transcendentals in both kernel and oracle) also projection, association
+  sets and TSDF values;
+* with the product math (CUDA atan2f/asinf vs numpy's SVML): >= 99.9 %
+  correspondence-mask agreement, poses within 1e-5 rad / 1e-5 m with equal
+  iteration counts, TSDF values within 1e-5.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PAIRS = ("room", "street", "synth")
+SENSOR_OF = {"room": "small", "street": "ouster", "synth": "synth"}
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import paper_2112_02779_b200 as rk
+    return rk
+
+
+def rot_err(Ra, Rb):
+    c = (np.trace(Ra.T @ Rb) - 1.0) / 2.0
+    return float(np.arccos(np.clip(c, -1.0, 1.0)))
+
+
+def set_agreement(a, b):
+    a, b = set(map(int, a)), set(map(int, b))
+    if not a and not b:
+        return 1.0
+    return len(a & b) / len(a | b)
+
+
+# ---------------------------------------------------------------- sensor model
+
+@pytest.mark.parametrize("name", ("small", "synth", "ouster"))
+def test_project_f32_cr_bitexact_vs_oracle(rk, name, sensors, osensors, golden_proj):
+    from paper_2112_02779_b200.lidar_model import MATH_CR
+    pts = golden_proj[f"{name}/p32_in"]
+    u, v, r, st = rk.project_many(pts, sensors[name], single=True, math=MATH_CR)
+    ou, ov, orr, ost = osensors[name].project_f32(pts, math="cr")
+    ok = ost == 0
+    assert np.array_equal(st, ost)
+    assert np.array_equal(v[ok], ov[ok]) and np.array_equal(u[ok], ou[ok])
+    assert np.array_equal(r, orr)
+
+
+@pytest.mark.parametrize("name", ("small", "synth", "ouster"))
+def test_project_f32_fast_vs_reference(rk, name, sensors, golden_proj):
+    g = golden_proj
+    pts = g[f"{name}/p32_in"]
+    u, v, r, st = rk.project_many(pts, sensors[name], single=True)
+    assert np.mean(st == g[f"{name}/p32_st"]) >= 0.999
+    both = (st == 0) & (g[f"{name}/p32_st"] == 0)
+    assert np.mean(v[both] == g[f"{name}/p32_v"][both]) >= 0.999
+    assert np.array_equal(r, g[f"{name}/p32_r"])           # no transcendental on r
+    du = np.abs(u[both] - g[f"{name}/p32_u"][both])
+    du = np.minimum(du, sensors[name].width - du)
+    assert np.percentile(du, 99.9) < 1e-3
+
+
+@pytest.mark.parametrize("name", ("small", "synth", "ouster"))
+def test_project_f64_vs_reference(rk, name, sensors, golden_proj):
+    g = golden_proj
+    u, v, r, st = rk.project_many(g[f"{name}/p64_in"], sensors[name])
+    assert np.mean(st == g[f"{name}/p64_st"]) >= 0.999
+    both = (st == 0) & (g[f"{name}/p64_st"] == 0)
+    assert np.mean(v[both] == g[f"{name}/p64_v"][both]) >= 0.999
+    same = both & (v == g[f"{name}/p64_v"])
+    assert np.abs(u[same] - g[f"{name}/p64_u"][same]).max() < 1e-9
+    assert np.abs(r - g[f"{name}/p64_r"]).max() < 1e-9
+
+
+@pytest.mark.parametrize("name", ("small", "synth", "ouster"))
+def test_rows_and_lookup_bitexact(rk, name, sensors, golden_proj):
+    g, intr = golden_proj, sensors[name]
+    assert np.array_equal(intr.row_from_elevation(g[f"{name}/phi64"]), g[f"{name}/row64"])
+    assert np.array_equal(intr.row_from_elevation(g[f"{name}/phi32"]), g[f"{name}/row32"])
+    assert np.array_equal(intr.inv_elevation_lut.lookup(g[f"{name}/phi64"]), g[f"{name}/lookup64"])
+
+
+# ---------------------------------------------------------------- images (K1, K2)
+
+@pytest.mark.parametrize("pair", PAIRS)
+def test_normals_bitexact(rk, pair, sensors, golden_icp):
+    img = rk.RangeImage(golden_icp[f"{pair}/dst"], sensors[SENSOR_OF[pair]])
+    nm = rk.compute_normal_map(img)
+    assert np.array_equal(nm.valid, golden_icp[f"{pair}/nvalid"])
+    assert np.array_equal(nm.vectors, golden_icp[f"{pair}/nrm"])
+
+
+@pytest.mark.parametrize("pair", ("room", "synth"))
+def test_point_clouds_and_pyramid_bitexact(rk, pair, sensors, osensors, golden_icp):
+    from oracle import image as oimg
+    from paper_2112_02779_b200.range_image import points_at_stride, stride_indices
+    intr = sensors[SENSOR_OF[pair]]
+    img = rk.RangeImage(golden_icp[f"{pair}/src"], intr)
+    assert np.array_equal(rk.to_point_cloud(img, 0.5, 20.0), golden_icp[f"{pair}/cloud"])
+    for s in (1, 2, 4):
+        assert np.array_equal(points_at_stride(img, s), golden_icp[f"{pair}/pts_s{s}"])
+        idx, _ = stride_indices(img, s, 0.5, 20.0)
+        v, u = oimg.stride_indices(golden_icp[f"{pair}/src"], s, 0.5, 20.0)
+        assert np.array_equal(idx.cpu().numpy(), v * intr.width + u)
+
+
+def test_pyramid_edge_cases(rk, sensors):
+    from paper_2112_02779_b200.range_image import stride_indices
+    intr = sensors["small"]
+    empty = rk.RangeImage(np.zeros((intr.height, intr.width), np.float32), intr)
+    for s in (1, 3, 4, 7):
+        idx, _ = stride_indices(empty, s)
+        assert idx.numel() == 0
+    full = rk.RangeImage(np.full((intr.height, intr.width), 5.0, np.float32), intr)
+    for s in (1, 3, 5, 33):
+        idx, _ = stride_indices(full, s)
+        Hs, Ws = -(-intr.height // s), -(-intr.width // s)
+        assert idx.numel() == Hs * Ws
+        vv, uu = np.meshgrid(np.arange(0, intr.height, s), np.arange(0, intr.width, s), indexing="ij")
+        assert np.array_equal(idx.cpu().numpy(), (vv * intr.width + uu).reshape(-1))
+
+
+# ---------------------------------------------------------------- association
+
+def _src_cloud(rk, pair, sensors, golden_icp):
+    return rk.to_point_cloud(rk.RangeImage(golden_icp[f"{pair}/src"], sensors[SENSOR_OF[pair]]))
+
+
+@pytest.mark.parametrize("pair", PAIRS)
+def test_correspondences_cr_bitexact_vs_oracle(rk, pair, sensors, osensors, golden_icp):
+    from oracle import icp as oicp
+    from paper_2112_02779_b200 import lidar_model as lm
+    g, intr = golden_icp, sensors[SENSOR_OF[pair]]
+    dst = rk.RangeImage(g[f"{pair}/dst"], intr)
+    nm = rk.compute_normal_map(dst)
+    src_pts = _src_cloud(rk, pair, sensors, golden_icp)
+    M = g[f"{pair}/corr_pose"]
+    pose = rk.RigidTransform(M[:3, :3], M[:3, 3])
+    lm.set_default_math(lm.MATH_CR)
+    try:
+        for s in (1, 2, 4):
+            c = rk.projective_correspondences(src_pts, dst, nm, pose, 0.5 * s, s, single=True)
+            sel, tgt, nrm, _ = oicp.correspondences_f32(osensors[SENSOR_OF[pair]], src_pts, g[f"{pair}/dst"],
+                                                        g[f"{pair}/nrm"], g[f"{pair}/nvalid"], M[:3, :3],
+                                                        M[:3, 3], 0.5 * s, s, math="cr")
+            assert np.array_equal(c.source, src_pts[sel])
+            assert np.array_equal(c.target, tgt) and np.array_equal(c.normal, nrm)
+    finally:
+        lm.set_default_math(lm.MATH_FAST)
+
+
+@pytest.mark.parametrize("pair", PAIRS)
+def test_correspondence_masks_vs_reference(rk, pair, sensors, golden_icp):
+    g, intr = golden_icp, sensors[SENSOR_OF[pair]]
+    dst = rk.RangeImage(g[f"{pair}/dst"], intr)
+    nm = rk.compute_normal_map(dst)
+    src_pts = _src_cloud(rk, pair, sensors, golden_icp)
+    M = g[f"{pair}/corr_pose"]
+    pose = rk.RigidTransform(M[:3, :3], M[:3, 3])
+    index = {tuple(r): i for i, r in enumerate(src_pts.tolist())}
+    for s in ((4,) if pair == "street" else (1, 2, 4)):
+        c = rk.projective_correspondences(src_pts, dst, nm, pose, 0.5 * s, s, single=True)
+        got = [index[tuple(r)] for r in c.source.tolist()]
+        assert set_agreement(got, g[f"{pair}/c32_s{s}_sel"]) >= 0.999
+    sub = src_pts[::7] if pair == "street" else src_pts[::2]
+    c = rk.projective_correspondences(sub, dst, nm, pose, 0.5, 1)
+    index = {tuple(r): i for i, r in enumerate(sub.tolist())}
+    got = np.array([index[tuple(r)] for r in c.source.tolist()])
+    assert set_agreement(got, g[f"{pair}/c64_sel"]) >= 0.999
+    common, ia, ib = np.intersect1d(got, g[f"{pair}/c64_sel"], return_indices=True)
+    assert np.abs(c.target[ia] - g[f"{pair}/c64_tgt"][ib]).max() < 1e-9
+
+
+# ---------------------------------------------------------------- registration (K3)
+
+@pytest.mark.parametrize("pair", PAIRS)
+def test_register_vs_reference(rk, pair, sensors, golden_icp):
+    g, intr = golden_icp, sensors[SENSOR_OF[pair]]
+    src, dst = rk.RangeImage(g[f"{pair}/src"], intr), rk.RangeImage(g[f"{pair}/dst"], intr)
+    res = rk.register(src, dst)
+    M = g[f"{pair}/reg_pose"]
+    stats = g[f"{pair}/reg_stats"]
+    assert res.converged == bool(g[f"{pair}/reg_converged"])
+    assert rot_err(res.pose.R, M[:3, :3]) < 1e-5
+    assert np.linalg.norm(res.pose.t - M[:3, 3]) < 1e-5
+    got = np.array([[s.stride, s.iteration, s.n_correspondences] for s in res.stats])
+    assert got.shape[0] == stats.shape[0]                      # same iteration count per level
+    assert np.array_equal(got[:, :2], stats[:, :2])
+    assert np.all(np.abs(got[:, 2] - stats[:, 2]) <= np.maximum(2, 1e-3 * stats[:, 2]))
+    cost = np.array([s.cost for s in res.stats])
+    assert np.allclose(cost, stats[:, 3], rtol=1e-3)
+
+
+@pytest.mark.parametrize("pair", PAIRS)
+def test_register_cr_vs_oracle(rk, pair, sensors, osensors, golden_icp):
+    from oracle import icp as oicp
+    from paper_2112_02779_b200 import lidar_model as lm
+    g, intr = golden_icp, sensors[SENSOR_OF[pair]]
+    src, dst = rk.RangeImage(g[f"{pair}/src"], intr), rk.RangeImage(g[f"{pair}/dst"], intr)
+    lm.set_default_math(lm.MATH_CR)
+    try:
+        res = rk.register(src, dst)
+    finally:
+        lm.set_default_math(lm.MATH_FAST)
+    ref = oicp.register(osensors[SENSOR_OF[pair]], g[f"{pair}/src"], g[f"{pair}/dst"], g[f"{pair}/nrm"],
+                        g[f"{pair}/nvalid"], math="cr")
+    assert res.converged == ref["converged"]
+    assert rot_err(res.pose.R, ref["R"]) < 1e-6 and np.linalg.norm(res.pose.t - ref["t"]) < 1e-6
+    assert [s.n_correspondences for s in res.stats] == [s[2] for s in ref["stats"]]
+
+
+def test_register_batch_deterministic_and_consistent(rk, sensors, golden_icp):
+    import torch
+    from paper_2112_02779_b200.range_image import normals_cross_batch
+    g, intr = golden_icp, sensors["ouster"]
+    src = torch.from_numpy(g["street/src"]).cuda()[None].repeat(8, 1, 1)
+    dst = torch.from_numpy(g["street/dst"]).cuda()[None].repeat(8, 1, 1)
+    surf = normals_cross_batch(intr, dst)
+    a = rk.register_batch(intr, src, dst, surf)
+    b = rk.register_batch(intr, src, dst, surf)
+    assert torch.equal(a.poses, b.poses)
+    assert bool((a.poses == a.poses[:1]).all())
+    single = rk.register(rk.RangeImage(g["street/src"], intr), rk.RangeImage(g["street/dst"], intr))
+    assert np.array_equal(a.pose(0).matrix(), single.pose.matrix())
+
+
+def test_register_nonconvergence_and_identity(rk, sensors, golden_icp):
+    intr = sensors["synth"]
+    img = rk.RangeImage(golden_icp["synth/dst"], intr)
+    empty = rk.RangeImage(np.zeros((intr.height, intr.width), np.float32), intr)
+    assert not rk.register(img, empty).converged
+    res = rk.register(img, img)
+    assert res.converged
+    assert rot_err(res.pose.R, np.eye(3)) < 1e-6 and np.linalg.norm(res.pose.t) < 1e-6
+
+
+def test_centroid_vs_reference(rk, sensors, golden_icp):
+    for pair in PAIRS:
+        intr = sensors[SENSOR_OF[pair]]
+        s = rk.to_point_cloud(rk.RangeImage(golden_icp[f"{pair}/src"], intr))
+        d = rk.to_point_cloud(rk.RangeImage(golden_icp[f"{pair}/dst"], intr))
+        t = rk.initial_translation_by_centroids(s, d).t
+        assert np.abs(t - golden_icp[f"{pair}/centroid_t"]).max() < 1e-12
+
+
+def test_gauss_newton_f64_helpers(rk):
+    from paper_2112_02779_b200 import registration as reg
+    g = np.random.default_rng(8)
+    p = g.normal(scale=3.0, size=(80, 3))
+    q = p + g.normal(scale=0.05, size=(80, 3))
+    n = g.normal(size=(80, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    corr = reg.CorrespondenceSet(p, q, n)
+    xi, _ = reg.gauss_newton_step(corr, rk.RigidTransform.identity(), 1e9)
+    r = reg.point_to_plane_residuals(corr, rk.RigidTransform.identity())
+    J = np.concatenate([np.cross(p, n), n], axis=1)
+    assert np.abs(xi - np.linalg.solve(J.T @ J, -J.T @ r)).max() < 1e-9
+    flat = np.zeros((100, 3))
+    flat[:, :2] = g.normal(scale=2.0, size=(100, 2))
+    plane = reg.CorrespondenceSet(flat, flat, np.tile([0.0, 0.0, 1.0], (100, 1)))
+    with pytest.raises(rk.DegenerateGeometry):
+        reg.gauss_newton_step(plane, rk.RigidTransform.identity(), 0.5)
+
+
+# ---------------------------------------------------------------- TSDF (K4, K5)
+
+def test_activation_bitexact(rk, golden_tsdf):
+    grid = rk.VoxelBlockGrid(voxel_size=0.1)
+    keys = rk.activate_blocks(golden_tsdf["act_pts"], grid, 0.55)
+    assert sorted(keys) == [tuple(k) for k in golden_tsdf["act_keys"].tolist()]
+    assert set(grid.blocks) == keys
+
+
+def _seq_grid(rk, sensors, g):
+    intr = sensors["small"]
+    grid = rk.VoxelBlockGrid(voxel_size=0.2)
+    counts = []
+    for f, M in zip(g["seq_frames"], g["seq_poses"]):
+        counts.append(rk.integrate_cloud_frame(grid, rk.RangeImage(f, intr),
+                                               rk.RigidTransform(M[:3, :3], M[:3, 3]), clip_max=12.0))
+    return grid, counts
+
+
+def _grid_vox(grid):
+    items = sorted(grid.blocks.items())
+    keys = [k for k, _ in items]
+    vox = np.stack([np.stack([b.tsdf.reshape(-1), b.weight.reshape(-1)], -1) for _, b in items])
+    return keys, vox
+
+
+def test_tsdf_sequence_cr_bitexact_vs_oracle(rk, sensors, osensors, golden_tsdf):
+    from oracle import tsdf as otsdf
+    from paper_2112_02779_b200 import lidar_model as lm
+    g = golden_tsdf
+    lm.set_default_math(lm.MATH_CR)
+    try:
+        grid, counts = _seq_grid(rk, sensors, g)
+    finally:
+        lm.set_default_math(lm.MATH_FAST)
+    og, oc = {}, []
+    for f, M in zip(g["seq_frames"], g["seq_poses"]):
+        oc.append(otsdf.integrate_cloud_frame(og, osensors["small"], f, M[:3, :3], M[:3, 3], 0.2, 0.8,
+                                              clip_max=12.0, math="cr")[1])
+    assert counts == oc
+    keys, vox = _grid_vox(grid)
+    assert keys == sorted(og)
+    ovox = np.stack([np.stack([og[k][0].reshape(-1), og[k][1].reshape(-1)], -1) for k in keys])
+    assert np.array_equal(vox, ovox)
+
+
+def test_tsdf_sequence_vs_reference(rk, sensors, golden_tsdf):
+    g = golden_tsdf
+    grid, counts = _seq_grid(rk, sensors, g)
+    keys, vox = _grid_vox(grid)
+    assert keys == [tuple(k) for k in g["seq_keys"].tolist()]            # bit-exact allocation
+    ref = g["seq_vox"]
+    assert np.mean(vox[..., 1] == ref[..., 1]) >= 0.9999
+    same_w = vox[..., 1] == ref[..., 1]
+    assert np.mean(np.abs(vox[..., 0] - ref[..., 0])[same_w] <= 1e-5) >= 0.9999
+    assert np.all(np.abs(np.array(counts) - g["seq_counts"]) <= np.maximum(3, 1e-3 * g["seq_counts"]))
+    s, w, ok = rk.query_sdf_many(grid, g["q_pts"])
+    assert np.mean(ok == g["q_ok"]) >= 0.99
+
+
+def test_tsdf_street_frame_vs_reference(rk, sensors, golden_tsdf, golden_icp):
+    g = golden_tsdf
+    grid = rk.VoxelBlockGrid(voxel_size=0.05)
+    n = rk.integrate_cloud_frame(grid, rk.RangeImage(golden_icp["street/dst"], sensors["ouster"]),
+                                 rk.RigidTransform.identity(), clip_max=30.0)
+    keys = sorted(grid.blocks)
+    assert keys == [tuple(k) for k in g["street_keys"].tolist()]
+    assert abs(n - int(g["street_count"])) <= 1e-4 * int(g["street_count"]) + 5
+    items = dict(grid.blocks.items())
+    for j, i in enumerate(g["street_pick"]):
+        b = items[keys[i]]
+        ref = g["street_pick_vox"][j]
+        assert np.mean(b.weight.reshape(-1) == ref[:, 1]) >= 0.999
+        assert np.mean(np.abs(b.tsdf.reshape(-1) - ref[:, 0]) <= 1e-5) >= 0.999
+
+
+def test_integrate_rejects_bad_pose(rk, sensors, golden_icp):
+    grid = rk.VoxelBlockGrid(voxel_size=0.1)
+    img = rk.RangeImage(golden_icp["synth/dst"], sensors["synth"])
+    with pytest.raises(rk.InvalidPose):
+        rk.integrate(grid, img, rk.RigidTransform(np.eye(3) * 2.0, np.zeros(3)), set())
+
+
+def test_block_mapping_roundtrip(rk):
+    grid = rk.VoxelBlockGrid(voxel_size=0.1)
+    blk = rk.VoxelBlock()
+    blk.tsdf = np.arange(4096, dtype=np.float32).reshape(16, 16, 16) / 4096
+    blk.weight = np.ones((16, 16, 16), np.float32)
+    grid.blocks[(1, -2, 3)] = blk
+    assert (1, -2, 3) in grid.blocks and len(grid.blocks) == 1
+    grid.reserve(4096)  # forces a flush + rehash
+    got = grid.blocks[(1, -2, 3)]
+    assert np.array_equal(got.tsdf, blk.tsdf) and np.array_equal(got.weight, blk.weight)
+
+
+# ---------------------------------------------------------------- marching cubes (K6)
+
+def _mesh_grid(rk, g):
+    grid = rk.VoxelBlockGrid(voxel_size=0.05, truncation=0.2)
+    for k, v in zip(g["sphere_keys"].tolist(), g["sphere_vox"]):
+        grid.blocks[tuple(k)] = rk.VoxelBlock(v[:, 0].reshape(16, 16, 16).copy(),
+                                              v[:, 1].reshape(16, 16, 16).copy())
+    return grid
+
+
+def test_mesh_sphere_vs_reference(rk, golden_mesh):
+    g = golden_mesh
+    m = rk.extract_mesh(_mesh_grid(rk, g))
+    V, T, N = g["sphere_V"], g["sphere_T"], g["sphere_N"]
+    assert m.n_vertices == V.shape[0] and m.n_triangles == T.shape[0]
+    pos = {tuple(p): i for i, p in enumerate(V.tolist())}
+    remap = np.array([pos[tuple(p)] for p in m.vertices.tolist()])       # exact positions
+    assert len(set(remap.tolist())) == V.shape[0]
+    assert np.abs(m.normals - N[remap]).max() < 1e-12
+    canon = lambda tris: {tuple(np.roll(t, -int(np.argmin(t)))) for t in tris.tolist()}  # noqa: E731
+    assert canon(remap[m.triangles]) == canon(T)
+
+
+def test_mesh_empty_and_uniform(rk):
+    grid = rk.VoxelBlockGrid(voxel_size=0.05)
+    m = rk.extract_mesh(grid)
+    assert m.n_vertices == 0 and m.n_triangles == 0
+    blk = rk.VoxelBlock(np.full((16, 16, 16), 0.2, np.float32), np.ones((16, 16, 16), np.float32))
+    grid.blocks[(0, 0, 0)] = blk
+    m = rk.extract_mesh(grid)
+    assert m.n_vertices == 0 and m.n_triangles == 0
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
