@@ -16,7 +16,7 @@ import numpy as np
 
 from .errors import STATUS_TO_ERROR, DeviceError
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "librkb200.so"
+LIB_PATH = Path(os.environ.get("RK_LIB") or Path(__file__).resolve().parent / "lib" / "librkb200.so")
 
 _p = C.c_void_p
 _i32 = C.c_int32

@@ -70,8 +70,45 @@ __device__ __forceinline__ bool associate(const SensorDev& s, const double* pose
   return d2 <= gate2;
 }
 
-template <int MATH, int NT>
-__global__ void __launch_bounds__(NT) k_register(IcpArgs A) {
+// Thread 0's per-iteration update (registration.py:266-282): the 6x6 checks,
+// the float64 solve, the twist update and the early-exit test.  Kept out of
+// line so its scratch arrays do not inflate the kernel's register budget.
+// Returns 0 iterate, 1 level done, 2 stop (status set).
+__device__ __noinline__ int solve_step(const double* tot, int n_corr, double* sh_pose,
+                                       const rk_icp_config* cfg, int* status, double* xi) {
+  if (n_corr < cfg->min_corr) {
+    *status = RK_ICP_TOO_FEW;
+    return 2;
+  }
+  double Hm[36], L[36], piv[6], b[6];
+  int q = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) { Hm[i * 6 + j] = Hm[j * 6 + i] = tot[q]; ++q; }
+  for (int i = 0; i < 6; ++i) b[i] = tot[21 + i];
+  bool ok = chol6(Hm, L, piv);
+  if (cond_exceeds6(Hm, L, ok, piv, 1e12)) {
+    *status = RK_ICP_DEGENERATE;
+    return 2;
+  }
+  chol_solve6(L, b, xi);
+  double P[12];
+  for (int i = 0; i < 12; ++i) P[i] = sh_pose[i];
+  se3_left_update(xi, P);
+  if (orth_defect(P) > 1e-12) reorthonormalize(P);
+  for (int i = 0; i < 12; ++i) sh_pose[i] = P[i];
+  const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+  const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+  return (nr < cfg->rot_eps && nt < cfg->trans_eps) ? 1 : 0;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+template <int MATH, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
   constexpr int NW = NT / 32;
   const int pair = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -83,6 +120,7 @@ __global__ void __launch_bounds__(NT) k_register(IcpArgs A) {
 
   __shared__ double sh_pose[12];
   __shared__ double sh_red[NW][kNumAcc];
+  __shared__ double sh_tot[kNumAcc];
   __shared__ int sh_cnt[NW];
   __shared__ int sh_ctrl;  // 0 iterate, 1 level done, 2 stop everything
   if (tid < 12) sh_pose[tid] = A.init12[pair * 12 + tid];
@@ -111,9 +149,14 @@ __global__ void __launch_bounds__(NT) k_register(IcpArgs A) {
       double cost = 0.0;
       float sumsq = 0.0f;
       int cnt = 0;
+      // row-major walk of the stride view without a per-point division
+      int vi = tid / Ws, ui = tid - (tid / Ws) * Ws;
+      const int dv = NT / Ws, du = NT - (NT / Ws) * Ws;
       for (int k = tid; k < npix; k += NT) {
-        const int vi = k / Ws;
-        const int v = vi * stride, u = (k - vi * Ws) * stride;
+        const int v = vi * stride, u = ui * stride;
+        vi += dv;
+        ui += du;
+        if (ui >= Ws) { ui -= Ws; ++vi; }
         const float r = __ldg(src + v * W + u);
         if (!range_ok(r, A.cfg.clip_min, A.cfg.clip_max)) continue;
         ++work;
@@ -147,67 +190,44 @@ __global__ void __launch_bounds__(NT) k_register(IcpArgs A) {
         sumsq = __fmaf_rn(res, res, sumsq);
         ++cnt;
       }
-      // ---- deterministic CTA reduction in float64
-      double red[kNumAcc];
+      // ---- deterministic CTA reduction in float64, one quantity at a time
 #pragma unroll
-      for (int i = 0; i < 27; ++i) red[i] = (double)acc[i];
-      red[27] = cost;
-      red[28] = (double)sumsq;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-        for (int i = 0; i < kNumAcc; ++i) red[i] += __shfl_xor_sync(0xffffffffu, red[i], off);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+      for (int i = 0; i < 27; ++i) {
+        const double v = warp_sum((double)acc[i]);
+        if (lane == 0) sh_red[warp][i] = v;
       }
-      if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < kNumAcc; ++i) sh_red[warp][i] = red[i];
-        sh_cnt[warp] = cnt;
+      {
+        const double c = warp_sum(cost);
+        const double q2 = warp_sum((double)sumsq);
+        const int n = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) {
+          sh_red[warp][27] = c;
+          sh_red[warp][28] = q2;
+          sh_cnt[warp] = n;
+        }
       }
       __syncthreads();
       if (tid < kNumAcc) {
         double t = 0.0;
         for (int w2 = 0; w2 < NW; ++w2) t += sh_red[w2][tid];
-        sh_red[0][tid] = t;
+        sh_tot[tid] = t;
       }
       __syncthreads();
       if (tid == 0) {
         int n_corr = 0;
         for (int w2 = 0; w2 < NW; ++w2) n_corr += sh_cnt[w2];
-        int ctrl = 0;
-        if (n_corr < A.cfg.min_corr) {
-          status = RK_ICP_TOO_FEW;
-          ctrl = 2;
-        } else {
-          double Hm[36], L[36], piv[6], b[6], xi[6];
-          int q = 0;
-          for (int i = 0; i < 6; ++i)
-            for (int j = i; j < 6; ++j) { Hm[i * 6 + j] = Hm[j * 6 + i] = sh_red[0][q]; ++q; }
-          for (int i = 0; i < 6; ++i) b[i] = sh_red[0][21 + i];
-          bool ok = chol6(Hm, L, piv);
-          if (cond_exceeds6(Hm, L, ok, piv, 1e12)) {
-            status = RK_ICP_DEGENERATE;
-            ctrl = 2;
-          } else {
-            chol_solve6(L, b, xi);
-            double P[12];
-            for (int i = 0; i < 12; ++i) P[i] = sh_pose[i];
-            se3_left_update(xi, P);
-            if (orth_defect(P) > 1e-12) reorthonormalize(P);
-            for (int i = 0; i < 12; ++i) sh_pose[i] = P[i];
-            if (A.stats && n_done < A.stats_stride) {
-              double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
-              row[0] = stride;
-              row[1] = it;
-              row[2] = n_corr;
-              row[3] = kern * kern * sh_red[0][27];
-              row[4] = sqrt(sh_red[0][28] / n_corr);
-            }
-            ++n_done;
-            const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
-            const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
-            if (nr < A.cfg.rot_eps && nt < A.cfg.trans_eps) ctrl = 1;
+        double xi[6];
+        const int ctrl = solve_step(sh_tot, n_corr, sh_pose, &A.cfg, &status, xi);
+        if (ctrl != 2) {
+          if (A.stats && n_done < A.stats_stride) {
+            double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
+            row[0] = stride;
+            row[1] = it;
+            row[2] = n_corr;
+            row[3] = kern * kern * sh_tot[27];
+            row[4] = sqrt(sh_tot[28] / n_corr);
           }
+          ++n_done;
         }
         sh_ctrl = ctrl;
       }
@@ -326,11 +346,14 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   a.stats_stride = stats ? stats_stride : 0;
   a.cfg = *cfg;
   a.pt_iters = pt_iters;
-  constexpr int NT = 256;
+#ifndef RK_ICP_MINB
+#define RK_ICP_MINB 3
+#endif
+  constexpr int NT = 256, MINB = RK_ICP_MINB;
   if (cfg->math == MATH_CR)
-    k_register<MATH_CR, NT><<<batch, NT, 0, S(stream)>>>(a);
+    k_register<MATH_CR, NT, MINB><<<batch, NT, 0, S(stream)>>>(a);
   else
-    k_register<MATH_FAST, NT><<<batch, NT, 0, S(stream)>>>(a);
+    k_register<MATH_FAST, NT, MINB><<<batch, NT, 0, S(stream)>>>(a);
   RK_LAUNCHED("k_register");
   return RK_OK;
 }
