@@ -19,236 +19,7 @@ static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p)
 
 namespace {
 
-struct IcpArgs {
-  SensorDev s;
-  const float* src_range;
-  const float* dst_range;
-  const float4* dst_surfel;
-  const int32_t* pair_src;
-  const int32_t* pair_dst;
-  const double* init12;
-  double* out12;
-  int32_t* status;
-  int32_t* n_iters;
-  double* stats;
-  int stats_stride;
-  rk_icp_config cfg;
-  unsigned long long* pt_iters;
-};
-
 constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
-
-// One source pixel's contribution (registration.py:145-187 + 339-354).
-// Returns false when the point has no surviving correspondence.
-template <int MATH>
-__device__ __forceinline__ bool associate(const SensorDev& s, const double* pose, const float4* surf,
-                                          int v, int u, float r, int stride, float inv_s,
-                                          float gate2, float& mx, float& my, float& mz, float& qx,
-                                          float& qy, float& qz, float4& nrm) {
-  double p[3], m[3];
-  unproject_px(s, v, u, r, p);
-  xform_rows(pose, pose + 9, p[0], p[1], p[2], m);
-  mx = (float)m[0];
-  my = (float)m[1];
-  mz = (float)m[2];
-  Proj32 pr = project_f32<MATH>(s, mx, my, mz);
-  if (pr.status != PROJ_OK) return false;
-  int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
-  if (col >= s.W) col = 0;
-  int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
-  if (row >= s.H) return false;  // dropped, not clamped (registration.py:157-159)
-  const int flat = row * s.W + col;
-  nrm = __ldg(surf + flat);
-  if (!(nrm.w > 0.0f)) return false;  // range > 0 and normal valid
-  float4 d = __ldg(s.dirs32 + flat);
-  float4 o = __ldg(s.origins32 + col);
-  qx = __fadd_rn(__fmul_rn(nrm.w, d.x), o.x);
-  qy = __fadd_rn(__fmul_rn(nrm.w, d.y), o.y);
-  qz = __fadd_rn(__fmul_rn(nrm.w, d.z), o.z);
-  float dx = __fsub_rn(mx, qx), dy = __fsub_rn(my, qy), dz = __fsub_rn(mz, qz);
-  float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-  return d2 <= gate2;
-}
-
-// Thread 0's per-iteration update (registration.py:266-282): the 6x6 checks,
-// the float64 solve, the twist update and the early-exit test.  Kept out of
-// line so its scratch arrays do not inflate the kernel's register budget.
-// Returns 0 iterate, 1 level done, 2 stop (status set).
-__device__ __noinline__ int solve_step(const double* tot, int n_corr, double* sh_pose,
-                                       const rk_icp_config* cfg, int* status, double* xi) {
-  if (n_corr < cfg->min_corr) {
-    *status = RK_ICP_TOO_FEW;
-    return 2;
-  }
-  double Hm[36], L[36], piv[6], b[6];
-  int q = 0;
-  for (int i = 0; i < 6; ++i)
-    for (int j = i; j < 6; ++j) { Hm[i * 6 + j] = Hm[j * 6 + i] = tot[q]; ++q; }
-  for (int i = 0; i < 6; ++i) b[i] = tot[21 + i];
-  bool ok = chol6(Hm, L, piv);
-  if (cond_exceeds6(Hm, L, ok, piv, 1e12)) {
-    *status = RK_ICP_DEGENERATE;
-    return 2;
-  }
-  chol_solve6(L, b, xi);
-  double P[12];
-  for (int i = 0; i < 12; ++i) P[i] = sh_pose[i];
-  se3_left_update(xi, P);
-  if (orth_defect(P) > 1e-12) reorthonormalize(P);
-  for (int i = 0; i < 12; ++i) sh_pose[i] = P[i];
-  const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
-  const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
-  return (nr < cfg->rot_eps && nt < cfg->trans_eps) ? 1 : 0;
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  return v;
-}
-
-template <int MATH, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
-  constexpr int NW = NT / 32;
-  const int pair = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const SensorDev& s = A.s;
-  const int H = s.H, W = s.W;
-  const size_t HW = (size_t)H * W;
-  const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
-  const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * HW;
-
-  __shared__ double sh_pose[12];
-  __shared__ double sh_red[NW][kNumAcc];
-  __shared__ double sh_tot[kNumAcc];
-  __shared__ int sh_cnt[NW];
-  __shared__ int sh_ctrl;  // 0 iterate, 1 level done, 2 stop everything
-  if (tid < 12) sh_pose[tid] = A.init12[pair * 12 + tid];
-  int n_done = 0, status = RK_ICP_CONVERGED;
-  unsigned work = 0;  // valid source points visited (all iterations)
-
-  for (int lv = 0; lv < A.cfg.n_levels; ++lv) {
-    const int stride = A.cfg.strides[lv];
-    const double level = A.cfg.scale_with_stride ? (double)stride : 1.0;
-    const double gate = A.cfg.max_dist * level;
-    const double kern = A.cfg.kernel_scale * level;
-    const float gate32 = (float)gate;
-    const float gate2 = __fmul_rn(gate32, gate32);
-    const float k32 = (float)kern;
-    const float inv_s = (float)(1.0 / stride);
-    const int Hs = (H + stride - 1) / stride, Ws = (W + stride - 1) / stride;
-    const int npix = Hs * Ws;
-    for (int it = 0; it < A.cfg.iters[lv]; ++it) {
-      __syncthreads();  // pose (and sh_ctrl reuse) ready
-      double pose[12];
-#pragma unroll
-      for (int i = 0; i < 12; ++i) pose[i] = sh_pose[i];
-      float acc[27];
-#pragma unroll
-      for (int i = 0; i < 27; ++i) acc[i] = 0.0f;
-      double cost = 0.0;
-      float sumsq = 0.0f;
-      int cnt = 0;
-      // row-major walk of the stride view without a per-point division
-      int vi = tid / Ws, ui = tid - (tid / Ws) * Ws;
-      const int dv = NT / Ws, du = NT - (NT / Ws) * Ws;
-      for (int k = tid; k < npix; k += NT) {
-        const int v = vi * stride, u = ui * stride;
-        vi += dv;
-        ui += du;
-        if (ui >= Ws) { ui -= Ws; ++vi; }
-        const float r = __ldg(src + v * W + u);
-        if (!range_ok(r, A.cfg.clip_min, A.cfg.clip_max)) continue;
-        ++work;
-        float mx, my, mz, qx, qy, qz;
-        float4 n;
-        if (!associate<MATH>(s, pose, surf, v, u, r, stride, inv_s, gate2, mx, my, mz, qx, qy, qz, n))
-          continue;
-        // residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352)
-        const float dx = __fsub_rn(mx, qx), dy = __fsub_rn(my, qy), dz = __fsub_rn(mz, qz);
-        const float res = __fadd_rn(__fadd_rn(__fmul_rn(n.x, dx), __fmul_rn(n.y, dy)), __fmul_rn(n.z, dz));
-        float J[6];
-        J[0] = __fsub_rn(__fmul_rn(my, n.z), __fmul_rn(mz, n.y));
-        J[1] = __fsub_rn(__fmul_rn(mz, n.x), __fmul_rn(mx, n.z));
-        J[2] = __fsub_rn(__fmul_rn(mx, n.y), __fmul_rn(my, n.x));
-        J[3] = n.x;
-        J[4] = n.y;
-        J[5] = n.z;
-        const float e = __fdiv_rn(res, k32);
-        const float w = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(1.0f, __fmul_rn(e, e))));
-        const float rw = -__fmul_rn(res, w);
-        int q = 0;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const float jw = __fmul_rn(J[i], w);
-#pragma unroll
-          for (int j = i; j < 6; ++j) { acc[q] = __fmaf_rn(jw, J[j], acc[q]); ++q; }
-        }
-#pragma unroll
-        for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
-        cost += (double)__fsub_rn(__fdiv_rn(1.0f, w), 1.0f);
-        sumsq = __fmaf_rn(res, res, sumsq);
-        ++cnt;
-      }
-      // ---- deterministic CTA reduction in float64, one quantity at a time
-#pragma unroll
-      for (int i = 0; i < 27; ++i) {
-        const double v = warp_sum((double)acc[i]);
-        if (lane == 0) sh_red[warp][i] = v;
-      }
-      {
-        const double c = warp_sum(cost);
-        const double q2 = warp_sum((double)sumsq);
-        const int n = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) {
-          sh_red[warp][27] = c;
-          sh_red[warp][28] = q2;
-          sh_cnt[warp] = n;
-        }
-      }
-      __syncthreads();
-      if (tid < kNumAcc) {
-        double t = 0.0;
-        for (int w2 = 0; w2 < NW; ++w2) t += sh_red[w2][tid];
-        sh_tot[tid] = t;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int n_corr = 0;
-        for (int w2 = 0; w2 < NW; ++w2) n_corr += sh_cnt[w2];
-        double xi[6];
-        const int ctrl = solve_step(sh_tot, n_corr, sh_pose, &A.cfg, &status, xi);
-        if (ctrl != 2) {
-          if (A.stats && n_done < A.stats_stride) {
-            double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
-            row[0] = stride;
-            row[1] = it;
-            row[2] = n_corr;
-            row[3] = kern * kern * sh_tot[27];
-            row[4] = sqrt(sh_tot[28] / n_corr);
-          }
-          ++n_done;
-        }
-        sh_ctrl = ctrl;
-      }
-      __syncthreads();
-      const int ctrl = sh_ctrl;
-      if (ctrl == 2) goto finish;
-      if (ctrl == 1) break;
-    }
-  }
-finish:
-  if (A.pt_iters) {
-    unsigned w = __reduce_add_sync(0xffffffffu, work);
-    if (lane == 0 && w) atomicAdd(A.pt_iters, (unsigned long long)w);
-  }
-  __syncthreads();
-  if (tid < 12) A.out12[pair * 12 + tid] = sh_pose[tid];
-  if (tid == 0) {
-    A.status[pair] = status;
-    A.n_iters[pair] = n_done;
-  }
-}
 
 // projective_correspondences(single=True) for an explicit float64 cloud
 template <int MATH>
@@ -314,49 +85,6 @@ extern "C" int rk_correspondences_f32(const rk_sensor* s, const double* src_pts,
   return RK_OK;
 }
 
-extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
-                                 const float* dst_surfel, const int32_t* pair_src,
-                                 const int32_t* pair_dst, int32_t batch, const double* init12,
-                                 const rk_icp_config* cfg, double* out12, int32_t* status,
-                                 int32_t* n_iters, double* stats, int32_t stats_stride,
-                                 unsigned long long* pt_iters, void* stream) {
-  (void)dst_range;
-  if (batch <= 0) return RK_OK;
-  if (!cfg || cfg->n_levels < 1 || cfg->n_levels > 8) {
-    rk_set_error("schedule must have 1..8 levels");
-    return RK_EGENERIC;
-  }
-  for (int l = 0; l < cfg->n_levels; ++l)
-    if (cfg->strides[l] < 1 || cfg->iters[l] < 1) {
-      rk_set_error("strides and iteration counts must be >= 1");
-      return RK_EGENERIC;
-    }
-  IcpArgs a;
-  a.s = s->dev;
-  a.src_range = src_range;
-  a.dst_range = dst_range;
-  a.dst_surfel = reinterpret_cast<const float4*>(dst_surfel);
-  a.pair_src = pair_src;
-  a.pair_dst = pair_dst;
-  a.init12 = init12;
-  a.out12 = out12;
-  a.status = status;
-  a.n_iters = n_iters;
-  a.stats = stats;
-  a.stats_stride = stats ? stats_stride : 0;
-  a.cfg = *cfg;
-  a.pt_iters = pt_iters;
-#ifndef RK_ICP_MINB
-#define RK_ICP_MINB 3
-#endif
-  constexpr int NT = 256, MINB = RK_ICP_MINB;
-  if (cfg->math == MATH_CR)
-    k_register<MATH_CR, NT, MINB><<<batch, NT, 0, S(stream)>>>(a);
-  else
-    k_register<MATH_FAST, NT, MINB><<<batch, NT, 0, S(stream)>>>(a);
-  RK_LAUNCHED("k_register");
-  return RK_OK;
-}
 
 // surfel map from an arbitrary NormalImage (vectors, valid) + range
 __global__ void k_make_surfel(const float* __restrict__ range, const float* __restrict__ nrm,

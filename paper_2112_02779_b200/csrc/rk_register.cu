@@ -1,0 +1,337 @@
+// rk_register.cu -- K3: the whole multi-scale projective point-to-plane ICP
+// schedule (registration.py:237-289) for a batch of independent pairs, one
+// launch.
+//
+// A "group" of WPP warps owns one registration pair for its whole schedule;
+// the pose lives in shared memory.  Every iteration each lane walks a
+// row-major slice of the stride-s source view straight out of the level-0
+// image (the reference's zero-copy StridedView, range_image.py:69-116),
+// associates it projectively (registration.py:117-187), and accumulates the
+// 21 + 6 normal-equation terms in float32 registers (the reference's sgemm
+// precision).  The group then reduces them in float64 with a fixed
+// shuffle/shared-memory tree -- deterministic, no float atomics -- and one
+// lane solves the 6x6 system, applies the twist and decides the early exit
+// (registration.py:261-282).
+//
+// WPP = 1 (warp per pair) is the throughput layout for large batches: no
+// CTA barriers, and a lane's serial solve stalls one warp while the SM's
+// other warps keep issuing.  WPP = 8 (CTA per pair) gives small batches
+// (odometry of one sequence) 8x more threads per pair.
+#include "rk_common.cuh"
+#include "rk_linalg.cuh"
+
+using namespace rk;
+
+static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+namespace {
+
+constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
+constexpr int kThreads = 256;
+
+struct IcpArgs {
+  SensorDev s;
+  const float* src_range;
+  const float4* dst_surfel;
+  const int32_t* pair_src;
+  const int32_t* pair_dst;
+  const double* init12;
+  double* out12;
+  int32_t* status;
+  int32_t* n_iters;
+  double* stats;
+  int stats_stride;
+  int batch;
+  rk_icp_config cfg;
+  unsigned long long* pt_iters;
+};
+
+// Per-iteration update by one lane (registration.py:266-282): the 6x6 checks,
+// the float64 solve, the twist update and the early-exit test.  Out of line so
+// its scratch arrays do not inflate the hot loop's register budget.
+// Returns 0 iterate, 1 level done, 2 stop (status set).
+__device__ __noinline__ int solve_step(const double* tot, int n_corr, double* pose,
+                                       const rk_icp_config* cfg, int* status) {
+  if (n_corr < cfg->min_corr) {
+    *status = RK_ICP_TOO_FEW;
+    return 2;
+  }
+  double Hm[36], L[36], piv[6], b[6], xi[6];
+  int q = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) { Hm[i * 6 + j] = Hm[j * 6 + i] = tot[q]; ++q; }
+  for (int i = 0; i < 6; ++i) b[i] = tot[21 + i];
+  bool ok = chol6(Hm, L, piv);
+  if (cond_exceeds6(Hm, L, ok, piv, 1e12)) {
+    *status = RK_ICP_DEGENERATE;
+    return 2;
+  }
+  chol_solve6(L, b, xi);
+  double P[12];
+  for (int i = 0; i < 12; ++i) P[i] = pose[i];
+  se3_left_update(xi, P);
+  if (orth_defect(P) > 1e-12) reorthonormalize(P);
+  for (int i = 0; i < 12; ++i) pose[i] = P[i];
+  const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+  const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+  return (nr < cfg->rot_eps && nt < cfg->trans_eps) ? 1 : 0;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+template <int WPP>
+__device__ __forceinline__ void group_sync(int g) {
+  if (WPP == 1) {
+    __syncwarp();
+  } else if (WPP * 32 == kThreads) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(WPP * 32) : "memory");
+  }
+}
+
+template <int MATH, int WPP, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
+  constexpr int NW = kThreads / 32, GROUPS = NW / WPP, GT = WPP * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = warp / WPP;
+  const int gtid = tid - g * GT;
+  const int pair = blockIdx.x * GROUPS + g;
+  if (pair >= A.batch) return;  // whole groups only (no CTA-wide barrier when GROUPS > 1)
+  const SensorDev& s = A.s;
+  const int H = s.H, W = s.W;
+  const size_t HW = (size_t)H * W;
+  const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
+  const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * HW;
+
+  __shared__ double sh_pose[GROUPS][12];
+  __shared__ double sh_red[NW][kNumAcc];
+  __shared__ double sh_tot[GROUPS][kNumAcc];
+  __shared__ int sh_cnt[NW];
+  __shared__ int sh_ctrl[GROUPS];
+  if (gtid < 12) sh_pose[g][gtid] = A.init12[pair * 12 + gtid];
+  int n_done = 0, status = RK_ICP_CONVERGED;
+  unsigned work = 0;  // valid source points visited (all iterations)
+  const float cmin = A.cfg.clip_min, cmax = A.cfg.clip_max;
+
+  for (int lv = 0; lv < A.cfg.n_levels; ++lv) {
+    const int stride = A.cfg.strides[lv];
+    const double level = A.cfg.scale_with_stride ? (double)stride : 1.0;
+    const double kern = A.cfg.kernel_scale * level;
+    const float gate32 = (float)(A.cfg.max_dist * level);
+    const float gate2 = __fmul_rn(gate32, gate32);
+    const float inv_k = (float)(1.0 / kern);
+    const float inv_s = (float)(1.0 / stride);
+    const int Hs = (H + stride - 1) / stride, Ws = (W + stride - 1) / stride;
+    const int npix = Hs * Ws;
+    const int dv = GT / Ws, du = GT - (GT / Ws) * Ws;
+    for (int it = 0; it < A.cfg.iters[lv]; ++it) {
+      group_sync<WPP>(g);  // pose (and sh_ctrl reuse) ready
+      double pose[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) pose[i] = sh_pose[g][i];
+      float acc[27];
+#pragma unroll
+      for (int i = 0; i < 27; ++i) acc[i] = 0.0f;
+      float cost = 0.0f, sumsq = 0.0f;
+      int cnt = 0;
+      // row-major walk of the stride view, next range prefetched one point ahead
+      int vi = gtid / Ws, ui = gtid - (gtid / Ws) * Ws;
+      float r_next = gtid < npix ? __ldg(src + vi * stride * W + ui * stride) : 0.0f;
+      for (int k = gtid; k < npix; k += GT) {
+        const int v = vi * stride, u = ui * stride;
+        const float r = r_next;
+        vi += dv;
+        ui += du;
+        if (ui >= Ws) { ui -= Ws; ++vi; }
+        if (k + GT < npix) r_next = __ldg(src + vi * stride * W + ui * stride);
+        if (!range_ok(r, cmin, cmax)) continue;
+        ++work;
+        // ---- association (registration.py:145-183), bit-exact float32/float64 restatement
+        double p[3], m[3];
+        unproject_px(s, v, u, r, p);
+        xform_rows(pose, pose + 9, p[0], p[1], p[2], m);
+        const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
+        const Proj32 pr = project_f32<MATH>(s, mx, my, mz);
+        if (pr.status != PROJ_OK) continue;
+        int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
+        if (col >= W) col = 0;
+        const int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
+        if (row >= H) continue;  // dropped, not clamped (registration.py:157-159)
+        const int flat = row * W + col;
+        const float4 n = __ldg(surf + flat);
+        const float4 d = __ldg(s.dirs32 + flat);
+        const float4 o = __ldg(s.origins32 + col);
+        if (!(n.w > 0.0f)) continue;  // stored range > 0 and normal valid
+        const float qx = __fadd_rn(__fmul_rn(n.w, d.x), o.x);
+        const float qy = __fadd_rn(__fmul_rn(n.w, d.y), o.y);
+        const float qz = __fadd_rn(__fmul_rn(n.w, d.z), o.z);
+        const float dx = __fsub_rn(mx, qx), dy = __fsub_rn(my, qy), dz = __fsub_rn(mz, qz);
+        const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+        if (!(d2 <= gate2)) continue;
+        // ---- residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352).
+        // Only the reduced sums matter here (pose tolerance 1e-5), so the
+        // weight uses the fast reciprocal square root.
+        const float res = __fadd_rn(__fadd_rn(__fmul_rn(n.x, dx), __fmul_rn(n.y, dy)), __fmul_rn(n.z, dz));
+        float J[6];
+        J[0] = __fsub_rn(__fmul_rn(my, n.z), __fmul_rn(mz, n.y));
+        J[1] = __fsub_rn(__fmul_rn(mz, n.x), __fmul_rn(mx, n.z));
+        J[2] = __fsub_rn(__fmul_rn(mx, n.y), __fmul_rn(my, n.x));
+        J[3] = n.x;
+        J[4] = n.y;
+        J[5] = n.z;
+        const float e = res * inv_k;
+        const float s1 = __fmaf_rn(e, e, 1.0f);
+        const float w = rsqrtf(s1);
+        const float rw = -res * w;
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const float jw = J[i] * w;
+#pragma unroll
+          for (int j = i; j < 6; ++j) { acc[q] = __fmaf_rn(jw, J[j], acc[q]); ++q; }
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
+        // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
+        cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
+        sumsq = __fmaf_rn(res, res, sumsq);
+        ++cnt;
+      }
+      // ---- deterministic group reduction in float64
+      double* tot = sh_tot[g];
+      if (WPP == 1) {
+#pragma unroll
+        for (int i = 0; i < 27; ++i) {
+          const double v = warp_sum((double)acc[i]);
+          if (lane == 0) tot[i] = v;
+        }
+        const double c = warp_sum((double)cost), q2 = warp_sum((double)sumsq);
+        const int nc = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) {
+          tot[27] = c;
+          tot[28] = q2;
+          sh_cnt[warp] = nc;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 27; ++i) {
+          const double v = warp_sum((double)acc[i]);
+          if (lane == 0) sh_red[warp][i] = v;
+        }
+        const double c = warp_sum((double)cost), q2 = warp_sum((double)sumsq);
+        const int nc = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) {
+          sh_red[warp][27] = c;
+          sh_red[warp][28] = q2;
+          sh_cnt[warp] = nc;
+        }
+        group_sync<WPP>(g);
+        if (gtid < kNumAcc) {
+          double t = 0.0;
+          for (int w2 = 0; w2 < WPP; ++w2) t += sh_red[g * WPP + w2][gtid];
+          tot[gtid] = t;
+        }
+        if (gtid == 0)
+          for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
+      }
+      group_sync<WPP>(g);
+      if (gtid == 0) {
+        const int n_corr = sh_cnt[g * WPP];
+        const int ctrl = solve_step(tot, n_corr, sh_pose[g], &A.cfg, &status);
+        if (ctrl != 2) {
+          if (A.stats && n_done < A.stats_stride) {
+            double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
+            row[0] = stride;
+            row[1] = it;
+            row[2] = n_corr;
+            row[3] = kern * kern * tot[27];
+            row[4] = sqrt(tot[28] / n_corr);
+          }
+          ++n_done;
+        }
+        sh_ctrl[g] = ctrl;
+      }
+      group_sync<WPP>(g);
+      const int ctrl = sh_ctrl[g];
+      if (ctrl == 2) goto finish;
+      if (ctrl == 1) break;
+    }
+  }
+finish:
+  if (A.pt_iters) {
+    const unsigned w = __reduce_add_sync(0xffffffffu, work);
+    if (lane == 0 && w) atomicAdd(A.pt_iters, (unsigned long long)w);
+  }
+  group_sync<WPP>(g);
+  if (gtid < 12) A.out12[pair * 12 + gtid] = sh_pose[g][gtid];
+  if (gtid == 0) {
+    A.status[pair] = status;
+    A.n_iters[pair] = n_done;
+  }
+}
+
+template <int MATH, int WPP, int MINB>
+int launch(const IcpArgs& a, cudaStream_t st) {
+  constexpr int GROUPS = kThreads / 32 / WPP;
+  const unsigned grid = (unsigned)((a.batch + GROUPS - 1) / GROUPS);
+  k_register<MATH, WPP, MINB><<<grid, kThreads, 0, st>>>(a);
+  RK_LAUNCHED("k_register");
+  return RK_OK;
+}
+
+}  // namespace
+
+#ifndef RK_ICP_MINB
+#define RK_ICP_MINB 3
+#endif
+
+extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
+                                 const float* dst_surfel, const int32_t* pair_src,
+                                 const int32_t* pair_dst, int32_t batch, const double* init12,
+                                 const rk_icp_config* cfg, double* out12, int32_t* status,
+                                 int32_t* n_iters, double* stats, int32_t stats_stride,
+                                 unsigned long long* pt_iters, void* stream) {
+  (void)dst_range;  // the surfel map carries the stored range of every valid pixel
+  if (batch <= 0) return RK_OK;
+  if (!cfg || cfg->n_levels < 1 || cfg->n_levels > 8) {
+    rk_set_error("schedule must have 1..8 levels");
+    return RK_EGENERIC;
+  }
+  for (int l = 0; l < cfg->n_levels; ++l)
+    if (cfg->strides[l] < 1 || cfg->iters[l] < 1) {
+      rk_set_error("strides and iteration counts must be >= 1");
+      return RK_EGENERIC;
+    }
+  IcpArgs a;
+  a.s = s->dev;
+  a.src_range = src_range;
+  a.dst_surfel = reinterpret_cast<const float4*>(dst_surfel);
+  a.pair_src = pair_src;
+  a.pair_dst = pair_dst;
+  a.init12 = init12;
+  a.out12 = out12;
+  a.status = status;
+  a.n_iters = n_iters;
+  a.stats = stats;
+  a.stats_stride = stats ? stats_stride : 0;
+  a.batch = batch;
+  a.cfg = *cfg;
+  a.pt_iters = pt_iters;
+  // warp-per-pair once the batch fills every warp slot of the GPU a few times
+  // over; CTA-per-pair for small batches (latency of a few pairs)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const char* force = getenv("RK_ICP_WPP");
+  const int wpp = force ? atoi(force) : (batch >= sms * 24 ? 1 : 8);
+  cudaStream_t st = S(stream);
+  constexpr int MINB = RK_ICP_MINB;
+  if (cfg->math == MATH_CR)
+    return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, 8, MINB>(a, st);
+  return wpp == 1 ? launch<MATH_FAST, 1, MINB>(a, st) : launch<MATH_FAST, 8, MINB>(a, st);
+}

@@ -230,6 +230,23 @@ def test_register_batch_deterministic_and_consistent(rk, sensors, golden_icp):
     assert np.array_equal(a.pose(0).matrix(), single.pose.matrix())
 
 
+@pytest.mark.parametrize("wpp", ("1", "8"))
+def test_register_batch_layouts_match_reference(rk, wpp, sensors, golden_icp, monkeypatch):
+    """Warp-per-pair and CTA-per-pair kernels both meet the reference contract."""
+    import torch
+    monkeypatch.setenv("RK_ICP_WPP", wpp)
+    g, intr = golden_icp, sensors["ouster"]
+    src = torch.from_numpy(g["street/src"]).cuda()[None].repeat(3, 1, 1)
+    dst = torch.from_numpy(g["street/dst"]).cuda()[None].repeat(3, 1, 1)
+    res = rk.register_batch(intr, src, dst, with_stats=True)
+    M = g["street/reg_pose"]
+    for b in range(3):
+        assert int(res.status[b]) == 0
+        assert int(res.iterations[b]) == g["street/reg_stats"].shape[0]
+        P = res.pose(b)
+        assert rot_err(P.R, M[:3, :3]) < 1e-5 and np.linalg.norm(P.t - M[:3, 3]) < 1e-5
+
+
 def test_register_nonconvergence_and_identity(rk, sensors, golden_icp):
     intr = sensors["synth"]
     img = rk.RangeImage(golden_icp["synth/dst"], intr)
