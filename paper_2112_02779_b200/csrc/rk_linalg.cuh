@@ -5,36 +5,40 @@
 
 namespace rk {
 
-// Cholesky H = L L^T (6x6, row-major).  Returns false on a non-positive pivot.
-__device__ inline bool chol6(const double* A, double* L, double* piv) {
+// Cholesky H = L L^T (6x6, row-major); dinv = 1 / diag(L), piv = diag(L)^2.
+// Returns false on a non-positive pivot.  Reciprocal diagonals keep the
+// single-lane solve to six float64 divisions.
+__device__ inline bool chol6(const double* A, double* L, double* piv, double* dinv) {
   for (int i = 0; i < 36; ++i) L[i] = 0.0;
   for (int j = 0; j < 6; ++j) {
     double d = A[j * 6 + j];
     for (int k = 0; k < j; ++k) d -= L[j * 6 + k] * L[j * 6 + k];
     if (!(d > 0.0)) return false;
     piv[j] = d;
-    double ljj = sqrt(d);
+    const double ljj = sqrt(d);
+    const double inv = 1.0 / ljj;
     L[j * 6 + j] = ljj;
+    dinv[j] = inv;
     for (int i = j + 1; i < 6; ++i) {
       double s = A[i * 6 + j];
       for (int k = 0; k < j; ++k) s -= L[i * 6 + k] * L[j * 6 + k];
-      L[i * 6 + j] = s / ljj;
+      L[i * 6 + j] = s * inv;
     }
   }
   return true;
 }
 
-__device__ inline void chol_solve6(const double* L, const double* b, double* x) {
+__device__ inline void chol_solve6(const double* L, const double* dinv, const double* b, double* x) {
   double y[6];
   for (int i = 0; i < 6; ++i) {
     double s = b[i];
     for (int k = 0; k < i; ++k) s -= L[i * 6 + k] * y[k];
-    y[i] = s / L[i * 6 + i];
+    y[i] = s * dinv[i];
   }
   for (int i = 5; i >= 0; --i) {
     double s = y[i];
     for (int k = i + 1; k < 6; ++k) s -= L[k * 6 + i] * x[k];
-    x[i] = s / L[i * 6 + i];
+    x[i] = s * dinv[i];
   }
 }
 
@@ -72,24 +76,32 @@ __device__ inline void jacobi_eig6(const double* A, double* ev) {
 }
 
 // numpy.linalg.cond(H) > thresh (2-norm, via singular values) for symmetric H.
-// Cheap exact screening: Cholesky pivots lie inside [lambda_min, lambda_max], so
-// max/min pivot <= cond; ||H||_F ||H^-1||_F >= cond.  Only the ambiguous band
-// between the two bounds pays for the Jacobi eigen solve.
-__device__ inline bool cond_exceeds6(const double* H, const double* L, bool chol_ok,
-                                     const double* piv, double thresh) {
+// Cheap exact screening: Cholesky pivots lie inside [lambda_min, lambda_max],
+// so max/min pivot <= cond; and ||H||_F * trace(H^-1) >= lambda_max/lambda_min
+// = cond, with trace(H^-1) = ||L^-1||_F^2.  Only the band between the two
+// bounds (a factor <= 6*sqrt(6)) pays for the Jacobi eigen solve.
+__device__ inline bool cond_exceeds6(const double* H, const double* L, const double* dinv,
+                                     bool chol_ok, const double* piv, double thresh) {
   if (chol_ok) {
     double pmax = piv[0], pmin = piv[0];
     for (int i = 1; i < 6; ++i) { pmax = fmax(pmax, piv[i]); pmin = fmin(pmin, piv[i]); }
-    if (pmax / pmin > thresh) return true;
-    double fh = 0.0, fi = 0.0;
+    if (pmax > thresh * pmin) return true;
+    double fh = 0.0;
     for (int i = 0; i < 36; ++i) fh += H[i] * H[i];
-    for (int c = 0; c < 6; ++c) {
-      double e[6] = {0, 0, 0, 0, 0, 0}, x[6];
-      e[c] = 1.0;
-      chol_solve6(L, e, x);
-      for (int i = 0; i < 6; ++i) fi += x[i] * x[i];
+    double M[36];  // L^-1, lower triangular
+    double tr = 0.0;
+    for (int i = 0; i < 6; ++i) {
+      M[i * 6 + i] = dinv[i];
+      tr += dinv[i] * dinv[i];
+      for (int j = 0; j < i; ++j) {
+        double s = 0.0;
+        for (int k = j; k < i; ++k) s += L[i * 6 + k] * M[k * 6 + j];
+        const double mij = -s * dinv[i];
+        M[i * 6 + j] = mij;
+        tr += mij * mij;
+      }
     }
-    if (sqrt(fh) * sqrt(fi) <= thresh) return false;
+    if (sqrt(fh) * tr <= thresh) return false;
   }
   double ev[6];
   jacobi_eig6(H, ev);

@@ -50,9 +50,9 @@ struct IcpArgs {
 // the float64 solve, the twist update and the early-exit test.  Out of line so
 // its scratch arrays do not inflate the hot loop's register budget.
 // Returns 0 iterate, 1 level done, 2 stop (status set).
-__device__ __noinline__ int solve_step(const double* tot, int n_corr, double* pose,
-                                       const rk_icp_config* cfg, int* status) {
-  if (n_corr < cfg->min_corr) {
+__device__ __noinline__ int solve_step(const double* tot, int n_corr, double* pose, int min_corr,
+                                       double rot_eps, double trans_eps, int* status) {
+  if (n_corr < min_corr) {
     *status = RK_ICP_TOO_FEW;
     return 2;
   }
@@ -61,12 +61,13 @@ __device__ __noinline__ int solve_step(const double* tot, int n_corr, double* po
   for (int i = 0; i < 6; ++i)
     for (int j = i; j < 6; ++j) { Hm[i * 6 + j] = Hm[j * 6 + i] = tot[q]; ++q; }
   for (int i = 0; i < 6; ++i) b[i] = tot[21 + i];
-  bool ok = chol6(Hm, L, piv);
-  if (cond_exceeds6(Hm, L, ok, piv, 1e12)) {
+  double dinv[6];
+  bool ok = chol6(Hm, L, piv, dinv);
+  if (cond_exceeds6(Hm, L, dinv, ok, piv, 1e12)) {
     *status = RK_ICP_DEGENERATE;
     return 2;
   }
-  chol_solve6(L, b, xi);
+  chol_solve6(L, dinv, b, xi);
   double P[12];
   for (int i = 0; i < 12; ++i) P[i] = pose[i];
   se3_left_update(xi, P);
@@ -74,7 +75,7 @@ __device__ __noinline__ int solve_step(const double* tot, int n_corr, double* po
   for (int i = 0; i < 12; ++i) pose[i] = P[i];
   const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
   const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
-  return (nr < cfg->rot_eps && nt < cfg->trans_eps) ? 1 : 0;
+  return (nr < rot_eps && nt < trans_eps) ? 1 : 0;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -131,9 +132,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     const int dv = GT / Ws, du = GT - (GT / Ws) * Ws;
     for (int it = 0; it < A.cfg.iters[lv]; ++it) {
       group_sync<WPP>(g);  // pose (and sh_ctrl reuse) ready
-      double pose[12];
-#pragma unroll
-      for (int i = 0; i < 12; ++i) pose[i] = sh_pose[g][i];
+      // the pose is read from shared memory at every use (broadcast LDS):
+      // holding it in registers would cost 24 of the 80 the occupancy allows
+      const double* pose = sh_pose[g];
       float acc[27];
 #pragma unroll
       for (int i = 0; i < 27; ++i) acc[i] = 0.0f;
@@ -142,18 +143,46 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       // row-major walk of the stride view, next range prefetched one point ahead
       int vi = gtid / Ws, ui = gtid - (gtid / Ws) * Ws;
       float r_next = gtid < npix ? __ldg(src + vi * stride * W + ui * stride) : 0.0f;
+#if RK_ICP_PREFETCH_DIRS
+      // the ray direction of the next pixel is pose-independent: fetch it with
+      // the range so the L2 latency overlaps the current point's work
+      double3 d_next = make_double3(0.0, 0.0, 0.0);
+      if (gtid < npix) {
+        const double* dp = s.dirs + 3 * ((size_t)vi * stride * W + ui * stride);
+        d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+      }
+#endif
       for (int k = gtid; k < npix; k += GT) {
         const int v = vi * stride, u = ui * stride;
         const float r = r_next;
+#if RK_ICP_PREFETCH_DIRS
+        const double3 dcur = d_next;
+#endif
         vi += dv;
         ui += du;
         if (ui >= Ws) { ui -= Ws; ++vi; }
-        if (k + GT < npix) r_next = __ldg(src + vi * stride * W + ui * stride);
+        if (k + GT < npix) {
+          r_next = __ldg(src + vi * stride * W + ui * stride);
+#if RK_ICP_PREFETCH_DIRS
+          const double* dp = s.dirs + 3 * ((size_t)vi * stride * W + ui * stride);
+          d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+#endif
+        }
         if (!range_ok(r, cmin, cmax)) continue;
         ++work;
         // ---- association (registration.py:145-183), bit-exact float32/float64 restatement
         double p[3], m[3];
+#if RK_ICP_PREFETCH_DIRS
+        {
+          const double rd = (double)r;
+          const double* o = s.origins + 3 * u;
+          p[0] = __dadd_rn(__dmul_rn(rd, dcur.x), __ldg(o + 0));
+          p[1] = __dadd_rn(__dmul_rn(rd, dcur.y), __ldg(o + 1));
+          p[2] = __dadd_rn(__dmul_rn(rd, dcur.z), __ldg(o + 2));
+        }
+#else
         unproject_px(s, v, u, r, p);
+#endif
         xform_rows(pose, pose + 9, p[0], p[1], p[2], m);
         const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
         const Proj32 pr = project_f32<MATH>(s, mx, my, mz);
@@ -242,7 +271,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       group_sync<WPP>(g);
       if (gtid == 0) {
         const int n_corr = sh_cnt[g * WPP];
-        const int ctrl = solve_step(tot, n_corr, sh_pose[g], &A.cfg, &status);
+        // (cfg fields by value: taking a kernel parameter's address would
+        // spill the whole argument block to local memory)
+        const int ctrl = solve_step(tot, n_corr, sh_pose[g], A.cfg.min_corr, A.cfg.rot_eps,
+                                    A.cfg.trans_eps, &status);
         if (ctrl != 2) {
           if (A.stats && n_done < A.stats_stride) {
             double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
@@ -286,6 +318,9 @@ int launch(const IcpArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+#ifndef RK_ICP_PREFETCH_DIRS
+#define RK_ICP_PREFETCH_DIRS 0
+#endif
 #ifndef RK_ICP_MINB
 #define RK_ICP_MINB 3
 #endif
@@ -333,5 +368,10 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   constexpr int MINB = RK_ICP_MINB;
   if (cfg->math == MATH_CR)
     return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, 8, MINB>(a, st);
-  return wpp == 1 ? launch<MATH_FAST, 1, MINB>(a, st) : launch<MATH_FAST, 8, MINB>(a, st);
+  switch (wpp) {
+    case 1: return launch<MATH_FAST, 1, MINB>(a, st);
+    case 2: return launch<MATH_FAST, 2, MINB>(a, st);
+    case 4: return launch<MATH_FAST, 4, MINB>(a, st);
+    default: return launch<MATH_FAST, 8, MINB>(a, st);
+  }
 }
