@@ -200,6 +200,16 @@ int rk_grid_set_touched(rk_grid* g, const int32_t* keys, int64_t n, void* stream
 int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* range,
                       const double* inv12, float clip_min, float clip_max, int math,
                       int64_t* updated, void* stream);
+/* multi-GPU hash sharding: the grid only allocates blocks whose
+ * owner(key) == rank; rk_block_owner is the host mirror of owner() for
+ * keys_host (n,3).  Sharded integration needs the frame's global touched
+ * count and largest key (the reference's sorted-chunk order): export the
+ * local pair with rk_grid_touch_stats, all-reduce (sum, max) across ranks and
+ * hand the device int64[2] back with rk_grid_set_global_touch (NULL = local). */
+int rk_grid_set_shard(rk_grid* g, int32_t rank, int32_t world);
+int rk_block_owner(const int32_t* keys_host, int64_t n, int32_t world, int32_t* owner_host);
+int rk_grid_touch_stats(rk_grid* g, int64_t* out2, void* stream);
+int rk_grid_set_global_touch(rk_grid* g, const int64_t* in2);
 /* export keys (n,3) int32 of every stored block, or of the touched list */
 int rk_grid_keys(rk_grid* g, int touched_only, int32_t* keys_out, int64_t cap,
                  int64_t* n_host, void* stream);

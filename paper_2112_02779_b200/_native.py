@@ -69,6 +69,10 @@ SIGNATURES = {
     "rk_grid_destroy": [_p],
     "rk_grid_reserve": [_p, _i64, _p],
     "rk_grid_clear": [_p, _p],
+    "rk_grid_set_shard": [_p, _i32, _i32],
+    "rk_block_owner": [_p, _i64, _i32, _p],
+    "rk_grid_touch_stats": [_p, _p, _p],
+    "rk_grid_set_global_touch": [_p, _p],
     "rk_grid_info": [_p, _p, _p],
     "rk_grid_activate_points": [_p, _p, _i64, _f64, _p],
     "rk_grid_activate_image": [_p, _p, _p, _p, _f64, _f32, _f32, _p],

@@ -13,10 +13,10 @@
 // lane solves the 6x6 system, applies the twist and decides the early exit
 // (registration.py:261-282).
 //
-// WPP = 1 (warp per pair) is the throughput layout for large batches: no
-// CTA barriers, and a lane's serial solve stalls one warp while the SM's
-// other warps keep issuing.  WPP = 8 (CTA per pair) gives small batches
-// (odometry of one sequence) 8x more threads per pair.
+// WPP = 8 (one 256-thread CTA per pair, 4 CTAs per SM) is the default: it
+// measured fastest at every batch size (fewer distinct pairs per SM keep the
+// surfel gathers cache-local).  WPP = 1/2/4 (several pairs per CTA, no
+// CTA-wide barrier) remain selectable with RK_ICP_WPP for experiments.
 #include "rk_common.cuh"
 #include "rk_linalg.cuh"
 
@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
 #endif
       for (int k = gtid; k < npix; k += GT) {
         const int v = vi * stride, u = ui * stride;
+        (void)v;
         const float r = r_next;
 #if RK_ICP_PREFETCH_DIRS
         const double3 dcur = d_next;
@@ -322,7 +323,7 @@ int launch(const IcpArgs& a, cudaStream_t st) {
 #define RK_ICP_PREFETCH_DIRS 0
 #endif
 #ifndef RK_ICP_MINB
-#define RK_ICP_MINB 3
+#define RK_ICP_MINB 4
 #endif
 
 extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
@@ -357,13 +358,12 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   a.batch = batch;
   a.cfg = *cfg;
   a.pt_iters = pt_iters;
-  // warp-per-pair once the batch fills every warp slot of the GPU a few times
-  // over; CTA-per-pair for small batches (latency of a few pairs)
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // CTA-per-pair (WPP = 8) measured fastest at every batch size on B200
+  // (profiles/README.md: 8 > 4 > 2 > 1 warps per pair at 16k pairs): fewer
+  // distinct pairs per SM keep each pair's surfel gathers L1/L2-local.
+  // RK_ICP_WPP=1|2|4 selects the other layouts for experiments.
   const char* force = getenv("RK_ICP_WPP");
-  const int wpp = force ? atoi(force) : (batch >= sms * 24 ? 1 : 8);
+  const int wpp = force ? atoi(force) : 8;
   cudaStream_t st = S(stream);
   constexpr int MINB = RK_ICP_MINB;
   if (cfg->math == MATH_CR)

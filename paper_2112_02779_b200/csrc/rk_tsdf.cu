@@ -62,7 +62,18 @@ struct GridDev {
   Counters* ctr;
   long long cap_blocks;
   unsigned long long hash_mask;
+  int shard_rank, shard_world;  // multi-GPU: this grid keeps owner(key) == rank
 };
+
+// owner of a block in a hash-sharded multi-GPU grid
+__host__ __device__ __forceinline__ unsigned long long owner_mix(unsigned long long k) {
+  k ^= k >> 31;
+  k *= 0x7fb5d329728ea185ull;
+  k ^= k >> 27;
+  k *= 0x81dadef4bc2dd44dull;
+  k ^= k >> 33;
+  return k;
+}
 
 // find or insert; returns hash position or -1 when the probe budget is spent
 __device__ long long hash_acquire(const GridDev& g, unsigned long long key, bool& inserted) {
@@ -95,6 +106,8 @@ __device__ long long hash_find(const GridDev& g, unsigned long long key) {
 // one touched key: insert, dedupe per frame, remember fresh keys
 __device__ __forceinline__ void touch_key(const GridDev& g, int frame, long long x, long long y, long long z) {
   unsigned long long key = pack_key(x, y, z);
+  if (g.shard_world > 1 && (int)(owner_mix(key) % (unsigned long long)g.shard_world) != g.shard_rank)
+    return;  // another GPU owns this block
   bool inserted;
   long long h = hash_acquire(g, key, inserted);
   if (h < 0) { atomicExch(&g.ctr->overflow, 1); return; }
@@ -211,6 +224,7 @@ struct IntegrateArgs {
   float tau, max_w, cmin, cmax;
   int free_space;
   long long* updated;
+  const long long* global_touch;  // sharded grids: {frame key count, max key} over all ranks
 };
 
 // K5: persistent CTAs walk the touched list; each block's 4096 voxels are
@@ -229,10 +243,14 @@ __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
   __syncthreads();
   const SensorDev& s = A.s;
   const int n_touched = A.g.ctr->n_touched;
-  const unsigned long long max_key = A.g.ctr->max_touched_key;
   // the reference integrates sorted keys in chunks of 146 blocks; a chunk of a
-  // single block goes through dgemv, which orders the FMA chain differently
-  const bool lone_tail = (n_touched % kChunkBlocks) == 1;
+  // single block goes through dgemv, which orders the FMA chain differently.
+  // A hash-sharded grid needs the frame's global count / largest key, which
+  // the caller all-reduces into global_touch = {count, max key}.
+  const long long n_all = A.global_touch ? A.global_touch[0] : n_touched;
+  const unsigned long long max_key =
+      A.global_touch ? (unsigned long long)A.global_touch[1] : A.g.ctr->max_touched_key;
+  const bool lone_tail = (n_all % kChunkBlocks) == 1;
   int count = 0;
   for (int e = blockIdx.x; e < n_touched; e += gridDim.x) {
     const int h = A.g.touched[e];
@@ -422,7 +440,26 @@ struct rk_grid {
   GridDev d;
   unsigned long long hash_cap;
   float* offsets;  // 4096*3
+  const long long* global_touch = nullptr;  // device {count, max key} (sharded grids)
 };
+
+// {n_touched, max touched key} of the last activation into a device int64[2]
+// (multi-GPU: all-reduce these with sum / max, then rk_grid_set_global_touch)
+__global__ void k_touch_stats(const Counters* c, long long* out) {
+  out[0] = c->n_touched;
+  out[1] = (long long)c->max_touched_key;
+}
+
+extern "C" int rk_grid_touch_stats(rk_grid* g, int64_t* out2, void* stream) {
+  k_touch_stats<<<1, 1, 0, S(stream)>>>(g->d.ctr, reinterpret_cast<long long*>(out2));
+  RK_LAUNCHED("k_touch_stats");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_set_global_touch(rk_grid* g, const int64_t* in2) {
+  g->global_touch = reinterpret_cast<const long long*>(in2);
+  return RK_OK;
+}
 
 static unsigned long long pow2_at_least(unsigned long long x) {
   unsigned long long p = 1024;
@@ -472,6 +509,8 @@ extern "C" int rk_grid_create(double voxel_size, double truncation, float max_we
   g->max_weight = max_weight;
   g->free_space = free_space;
   g->frame = 1;
+  g->d.shard_rank = 0;
+  g->d.shard_world = 1;
   if (capacity_blocks < 64) capacity_blocks = 64;
   int rc = alloc_tables(g, capacity_blocks, 0);
   if (rc) { delete g; return rc; }
@@ -591,6 +630,7 @@ extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* ra
   a.cmax = clip_max;
   a.free_space = g->free_space;
   a.updated = reinterpret_cast<long long*>(updated);
+  a.global_touch = g->global_touch;
   constexpr int NT = 256;
   const unsigned grid = 148 * 4;
   const size_t smem = kVox * 3 * sizeof(float);
@@ -697,5 +737,26 @@ extern "C" int rk_grid_clear(rk_grid* g, void* stream) {
   k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr);
   RK_LAUNCHED("rk_grid_clear");
   g->frame += 1;
+  return RK_OK;
+}
+
+// multi-GPU hash sharding: from now on this grid only allocates blocks with
+// owner_mix(packed key) % world == rank
+extern "C" int rk_grid_set_shard(rk_grid* g, int32_t rank, int32_t world) {
+  if (world < 1 || rank < 0 || rank >= world) {
+    rk_set_error("bad shard rank %d / world %d", rank, world);
+    return RK_EGENERIC;
+  }
+  g->d.shard_rank = rank;
+  g->d.shard_world = world;
+  return RK_OK;
+}
+
+// host mirror of the device owner function (for tests / host-side routing)
+extern "C" int rk_block_owner(const int32_t* keys_host, int64_t n, int32_t world, int32_t* owner_host) {
+  for (int64_t i = 0; i < n; ++i) {
+    unsigned long long key = pack_key(keys_host[3 * i], keys_host[3 * i + 1], keys_host[3 * i + 2]);
+    owner_host[i] = (int32_t)(owner_mix(key) % (unsigned long long)world);
+  }
   return RK_OK;
 }

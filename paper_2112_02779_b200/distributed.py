@@ -1,0 +1,159 @@
+"""One process per GPU (torch.distributed over NCCL/NVLink) for the paths that
+shard:
+
+* ICP: independent pairs are split into contiguous slices (``shard``); the
+  only collective is the final pose all-gather (``all_gather_varsize``).
+* TSDF: voxel blocks are hash-sharded across ranks -- rank r allocates and
+  integrates only blocks with ``owner(key) == r`` (``rk_grid_set_shard``).
+  Per frame the range image + pose are broadcast once; the frame's touched
+  count / largest key are reduced so every rank reproduces the reference's
+  sorted-chunk arithmetic; before meshing every rank's blocks are gathered.
+
+The communication helpers take plain tensors so they run under the ``gloo``
+backend on CPU as well (tests/test_distributed.py); ``ShardedGrid`` adds the
+device grid on top.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import _native as nat
+
+
+def init_from_env(backend: str | None = None):
+    """torch.distributed from torchrun's env (RANK/WORLD_SIZE/MASTER_*);
+    returns (dist or None, rank, world)."""
+    if "RANK" not in os.environ or int(os.environ.get("WORLD_SIZE", "1")) <= 1:
+        return None, 0, 1
+    import torch
+    import torch.distributed as dist
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    if not dist.is_initialized():
+        dist.init_process_group(backend)
+    return dist, dist.get_rank(), dist.get_world_size()
+
+
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) slice of n independent units for one rank; slices
+    differ in size by at most one and cover 0..n exactly."""
+    base, extra = divmod(int(n), int(world))
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def all_gather_varsize(t, dist=None):
+    """All-gather tensors whose first dimension differs per rank (counts
+    first, then one padded all_gather); returns the concatenation in rank order."""
+    import torch
+    import torch.distributed as tdist
+    d = dist or tdist
+    world = d.get_world_size()
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    d.all_gather(counts, n)
+    counts = [int(c.item()) for c in counts]
+    width = max(counts) if counts else 0
+    pad = torch.zeros((width,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[:t.shape[0]] = t
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    d.all_gather(bufs, pad)
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)])
+
+
+def broadcast_frames(frames, poses, src: int = 0, dist=None):
+    """Broadcast (F,H,W) float32 frames and (F,12) float64 poses from src."""
+    import torch.distributed as tdist
+    d = dist or tdist
+    d.broadcast(frames, src)
+    d.broadcast(poses, src)
+    return frames, poses
+
+
+def reduce_touch_stats(stats, dist=None):
+    """{local touched count, local max key} -> {global count, global max key}
+    (int64[2] tensor, in place)."""
+    import torch
+    import torch.distributed as tdist
+    d = dist or tdist
+    world = d.get_world_size()
+    bufs = [torch.empty_like(stats) for _ in range(world)]
+    d.all_gather(bufs, stats)
+    allv = torch.stack(bufs)
+    stats[0] = allv[:, 0].sum()
+    stats[1] = allv[:, 1].max()
+    return stats
+
+
+def block_owner(keys, world: int) -> np.ndarray:
+    """Owning rank of each block key (host mirror of the device owner hash)."""
+    k = np.ascontiguousarray(np.asarray(keys, dtype=np.int32).reshape(-1, 3))
+    out = np.empty(k.shape[0], dtype=np.int32)
+    nat.call("rk_block_owner", k.ctypes.data, k.shape[0], int(world), out.ctypes.data)
+    return out
+
+
+class ShardedGrid:
+    """A VoxelBlockGrid whose blocks are hash-sharded over the ranks."""
+
+    def __init__(self, voxel_size, rank, world, dist=None, **grid_kw):
+        from .sdf_volume import VoxelBlockGrid
+        self.grid = VoxelBlockGrid(voxel_size=voxel_size, **grid_kw)
+        self.rank, self.world, self.dist = rank, world, dist
+        nat.call("rk_grid_set_shard", self.grid._ensure(), int(rank), int(world))
+        self._touch = nat.zeros((2,), np.int64)
+        if world > 1:
+            nat.call("rk_grid_set_global_touch", self.grid._handle, nat.ptr(self._touch))
+
+    def integrate_frames(self, intr, frames, poses_w, inv_w, clip_min=0.0, clip_max=np.inf,
+                         updated=None):
+        """integrate_cloud_frame for F frames on this rank's shard.  frames /
+        poses must already be identical on every rank (see broadcast_frames)."""
+        from . import lidar_model as lm
+        g = self.grid
+        h = g._prepare()
+        sensor = lm.device_sensor(intr)
+        if updated is None:
+            updated = nat.zeros((1,), np.int64)
+        st = nat.stream_ptr()
+        cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
+        for f in range(frames.shape[0]):
+            nat.call("rk_grid_activate_image", h, sensor, nat.ptr(frames[f]), nat.ptr(poses_w[f]),
+                     float(g.truncation), cmin, cmax, st)
+            if self.world > 1:
+                nat.call("rk_grid_touch_stats", h, nat.ptr(self._touch), st)
+                reduce_touch_stats(self._touch, self.dist)
+            nat.call("rk_grid_integrate", h, sensor, nat.ptr(frames[f]), nat.ptr(inv_w[f]), cmin, cmax,
+                     lm.default_math(), nat.ptr(updated), st)
+        g.blocks._bump()
+        return updated
+
+    def gather_blocks(self):
+        """All ranks' (keys (n,3) int32, voxels (n,4096,2) float32), device, rank order."""
+        g = self.grid
+        keys = nat.to_dev(g._export_keys(touched=False), np.int32)
+        vox = nat.empty((keys.shape[0], 4096, 2), np.float32)
+        if keys.shape[0]:
+            nat.call("rk_grid_read_blocks", g._handle, nat.ptr(keys), keys.shape[0], nat.ptr(vox), None,
+                     nat.stream_ptr())
+        if self.world == 1:
+            return keys, vox
+        return all_gather_varsize(keys, self.dist), all_gather_varsize(vox, self.dist)
+
+    def merged_grid(self):
+        """A single-device grid holding every rank's blocks (for meshing)."""
+        from .sdf_volume import VoxelBlockGrid
+        keys, vox = self.gather_blocks()
+        n = int(keys.shape[0])
+        out = VoxelBlockGrid(voxel_size=self.grid.voxel_size, truncation=self.grid.truncation,
+                             max_weight=self.grid.max_weight, capacity=max(1024, 2 * n))
+        if n:
+            nat.call("rk_grid_write_blocks", out._ensure(), nat.ptr(keys.contiguous()), n,
+                     nat.ptr(vox.contiguous()), nat.stream_ptr())
+            out.blocks._bump()
+        return out

@@ -15,6 +15,7 @@ import numpy as np
 
 from . import _native as nat
 from . import lidar_model as lm
+from .distributed import all_gather_varsize, shard  # noqa: F401  (re-exported)
 from .sdf_volume import VoxelBlockGrid
 from .se3 import RigidTransform
 
@@ -99,24 +100,7 @@ def clear_grid(grid: VoxelBlockGrid):
     grid.blocks._bump()
 
 
-def shard(n: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous [lo, hi) slice of n independent units for one rank."""
-    base, extra = divmod(n, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
-
-
-def gather_poses(local_poses, n_total: int, rank: int, world: int):
-    """All-gather per-rank (n_i, 12) pose slices into (n_total, 12) on every
-    rank (torch.distributed; the only cross-rank traffic of the ICP batch)."""
-    t = nat.torch()
-    import torch.distributed as dist
-    if world == 1:
-        return local_poses
-    sizes = [shard(n_total, r, world) for r in range(world)]
-    width = max(hi - lo for lo, hi in sizes)
-    pad = t.zeros((width, local_poses.shape[1]), dtype=local_poses.dtype, device=local_poses.device)
-    pad[:local_poses.shape[0]] = local_poses
-    bufs = [t.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad)
-    return t.cat([b[:hi - lo] for b, (lo, hi) in zip(bufs, sizes)])
+def gather_poses(local_poses, world: int):
+    """All-gather per-rank (n_i, 12) pose slices (rank order) -- the only
+    cross-rank traffic of a sharded ICP batch."""
+    return local_poses if world == 1 else all_gather_varsize(local_poses)

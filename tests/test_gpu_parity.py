@@ -361,6 +361,44 @@ def test_tsdf_street_frame_vs_reference(rk, sensors, golden_tsdf, golden_icp):
         assert np.mean(np.abs(b.tsdf.reshape(-1) - ref[:, 0]) <= 1e-5) >= 0.999
 
 
+def test_hash_sharded_grid_equals_single_grid(rk, sensors, golden_icp):
+    """Two block shards (emulated in one process) reproduce the unsharded grid
+    bit for bit, including the global sorted-chunk arithmetic."""
+    import torch
+    from paper_2112_02779_b200 import _native as nat
+    from paper_2112_02779_b200 import lidar_model as lm
+    intr = sensors["ouster"]
+    frame = torch.from_numpy(golden_icp["street/dst"]).cuda()
+    pose = rk.RigidTransform.identity()
+    full = rk.VoxelBlockGrid(voxel_size=0.05, capacity=8192)
+    n_full = rk.integrate_cloud_frame(full, rk.RangeImage(frame, intr), pose, clip_max=30.0)
+    shards = [rk.VoxelBlockGrid(voxel_size=0.05, capacity=8192) for _ in range(2)]
+    st = nat.stream_ptr()
+    p12 = nat.to_dev(pose.as_row12(), np.float64)
+    inv = nat.to_dev(pose.inverse().as_row12(), np.float64)
+    stats = [nat.zeros((2,), np.int64) for _ in range(2)]
+    for r, g in enumerate(shards):
+        h = g._ensure()
+        nat.call("rk_grid_set_shard", h, r, 2)
+        nat.call("rk_grid_activate_image", h, lm.device_sensor(intr), nat.ptr(frame), nat.ptr(p12),
+                 float(g.truncation), 0.0, 30.0, st)
+        nat.call("rk_grid_touch_stats", h, nat.ptr(stats[r]), st)
+    glob = torch.stack([stats[0][0] + stats[1][0], torch.maximum(stats[0][1], stats[1][1])])
+    upd = nat.zeros((1,), np.int64)
+    for g in shards:
+        nat.call("rk_grid_set_global_touch", g._handle, nat.ptr(glob))
+        nat.call("rk_grid_integrate", g._handle, lm.device_sensor(intr), nat.ptr(frame), nat.ptr(inv),
+                 0.0, 30.0, lm.default_math(), nat.ptr(upd), st)
+        g.blocks._bump()
+    assert int(upd.item()) == n_full
+    k0, k1 = set(shards[0].blocks), set(shards[1].blocks)
+    assert not (k0 & k1) and (k0 | k1) == set(full.blocks)
+    fb = dict(full.blocks.items())
+    for g in shards:
+        for k, b in g.blocks.items():
+            assert np.array_equal(b.tsdf, fb[k].tsdf) and np.array_equal(b.weight, fb[k].weight)
+
+
 def test_integrate_rejects_bad_pose(rk, sensors, golden_icp):
     grid = rk.VoxelBlockGrid(voxel_size=0.1)
     img = rk.RangeImage(golden_icp["synth/dst"], sensors["synth"])
