@@ -38,8 +38,11 @@ enum {
   RK_ECAPACITY = -11        /* voxel-block pool full (caller grows, retries) */
 };
 
-/* math modes for the float32 transcendentals */
-enum { RK_MATH_FAST = 0, RK_MATH_CR = 1 };
+/* math modes of the float32 projection:
+ * FAST = minimax atan2/asin + reciprocal refinements (default), CR = float64
+ * transcendentals rounded once (bit-comparable with the oracle), LIBM = CUDA's
+ * accurate atan2f/asinf with IEEE division (only rk_project_f32 accepts it). */
+enum { RK_MATH_FAST = 0, RK_MATH_CR = 1, RK_MATH_LIBM = 2 };
 
 /* per-pair ICP status (registration.py:266-272) */
 enum { RK_ICP_CONVERGED = 0, RK_ICP_TOO_FEW = 1, RK_ICP_DEGENERATE = 2 };

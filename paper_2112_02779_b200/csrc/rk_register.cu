@@ -22,6 +22,13 @@
 
 using namespace rk;
 
+#ifndef RK_ICP_MINB
+#define RK_ICP_MINB 4
+#endif
+#ifndef RK_ICP_PREFETCH_DIRS
+#define RK_ICP_PREFETCH_DIRS 1
+#endif
+
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
 namespace {
@@ -95,15 +102,23 @@ __device__ __forceinline__ void group_sync(int g) {
   }
 }
 
-template <int MATH, int WPP, int MINB>
+// STATS: accumulate the robust cost and squared residuals (IterationStats
+// rows); the pose update needs neither, so batch runs without stats skip them.
+template <int MATH, int WPP, int MINB, bool SMEM, bool STATS>
 __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   constexpr int NW = kThreads / 32, GROUPS = NW / WPP, GT = WPP * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp / WPP;
   const int gtid = tid - g * GT;
   const int pair = blockIdx.x * GROUPS + g;
-  if (pair >= A.batch) return;  // whole groups only (no CTA-wide barrier when GROUPS > 1)
   const SensorDev& s = A.s;
+  __shared__ RowTablesSmem sh_tab;
+  if (SMEM) {
+    stage_tables(s, sh_tab, tid, kThreads);
+    __syncthreads();
+  }
+  if (pair >= A.batch) return;  // whole groups only (no CTA-wide barrier when GROUPS > 1)
+  const RowTables tb = SMEM ? RowTables{sh_tab.el32, sh_tab.az32, sh_tab.inv_rows} : global_tables(s);
   const int H = s.H, W = s.W;
   const size_t HW = (size_t)H * W;
   const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
@@ -116,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   __shared__ int sh_ctrl[GROUPS];
   if (gtid < 12) sh_pose[g][gtid] = A.init12[pair * 12 + gtid];
   int n_done = 0, status = RK_ICP_CONVERGED;
-  unsigned work = 0;  // valid source points visited (all iterations)
+  unsigned work = 0;  // valid source points visited (all iterations), per thread
   const float cmin = A.cfg.clip_min, cmax = A.cfg.clip_max;
 
   for (int lv = 0; lv < A.cfg.n_levels; ++lv) {
@@ -129,51 +144,75 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     const float inv_s = (float)(1.0 / stride);
     const int Hs = (H + stride - 1) / stride, Ws = (W + stride - 1) / stride;
     const int npix = Hs * Ws;
-    const int dv = GT / Ws, du = GT - (GT / Ws) * Ws;
+    // row-major walk of the stride view (the reference's zero-copy StridedView,
+    // range_image.py:69-116) by GT-point steps, as running pixel offsets:
+    // one step advances (dv rows, du view columns), wrapping at Ws
+    const int dv = GT / Ws, du = GT - dv * Ws;
+    const int step_off = dv * stride * W + du * stride;
+    const int wrap_off = stride * W - Ws * stride;
+    const int vi0 = gtid / Ws, ui0 = gtid - vi0 * Ws;
+    const int off0 = vi0 * stride * W + ui0 * stride;
+    // executed work (the roofline's unit) = valid points of this level x the
+    // iterations run; counted once per level, outside the hot loop
+    unsigned valid_lv = 0;
+    if (A.pt_iters) {
+      int off = off0, ui = ui0;
+      for (int k = gtid; k < npix; k += GT) {
+        valid_lv += range_ok(__ldg(src + off), cmin, cmax) ? 1u : 0u;
+        off += step_off;
+        ui += du;
+        if (ui >= Ws) { ui -= Ws; off += wrap_off; }
+      }
+    }
+    int executed = 0;
     for (int it = 0; it < A.cfg.iters[lv]; ++it) {
+      ++executed;
       group_sync<WPP>(g);  // pose (and sh_ctrl reuse) ready
       // the pose is read from shared memory at every use (broadcast LDS):
-      // holding it in registers would cost 24 of the 80 the occupancy allows
+      // holding it in registers would cost 24 of the registers the occupancy allows
       const double* pose = sh_pose[g];
       float acc[27];
 #pragma unroll
       for (int i = 0; i < 27; ++i) acc[i] = 0.0f;
       float cost = 0.0f, sumsq = 0.0f;
       int cnt = 0;
-      // row-major walk of the stride view, next range prefetched one point ahead
-      int vi = gtid / Ws, ui = gtid - (gtid / Ws) * Ws;
-      float r_next = gtid < npix ? __ldg(src + vi * stride * W + ui * stride) : 0.0f;
+      int off = off0, ui = ui0;
+      // the next point's range (and, with RK_ICP_PREFETCH_DIRS, its ray) is
+      // pose-independent: fetched one point ahead so the latency overlaps the
+      // current point's math
+      float r_next = 0.0f;
 #if RK_ICP_PREFETCH_DIRS
-      // the ray direction of the next pixel is pose-independent: fetch it with
-      // the range so the L2 latency overlaps the current point's work
       double3 d_next = make_double3(0.0, 0.0, 0.0);
-      if (gtid < npix) {
-        const double* dp = s.dirs + 3 * ((size_t)vi * stride * W + ui * stride);
-        d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
-      }
 #endif
+      if (gtid < npix) {
+        r_next = __ldg(src + off);
+#if RK_ICP_PREFETCH_DIRS
+        const double* dp = s.dirs + 3 * (size_t)off;
+        d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+#endif
+      }
       for (int k = gtid; k < npix; k += GT) {
-        const int v = vi * stride, u = ui * stride;
-        (void)v;
         const float r = r_next;
 #if RK_ICP_PREFETCH_DIRS
         const double3 dcur = d_next;
+#else
+        const double* dcp = s.dirs + 3 * (size_t)off;
+        const double3 dcur = make_double3(__ldg(dcp), __ldg(dcp + 1), __ldg(dcp + 2));
 #endif
-        vi += dv;
+        const int u = ui * stride;
+        off += step_off;
         ui += du;
-        if (ui >= Ws) { ui -= Ws; ++vi; }
+        if (ui >= Ws) { ui -= Ws; off += wrap_off; }
         if (k + GT < npix) {
-          r_next = __ldg(src + vi * stride * W + ui * stride);
+          r_next = __ldg(src + off);
 #if RK_ICP_PREFETCH_DIRS
-          const double* dp = s.dirs + 3 * ((size_t)vi * stride * W + ui * stride);
+          const double* dp = s.dirs + 3 * (size_t)off;
           d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
 #endif
         }
         if (!range_ok(r, cmin, cmax)) continue;
-        ++work;
         // ---- association (registration.py:145-183), bit-exact float32/float64 restatement
         double p[3], m[3];
-#if RK_ICP_PREFETCH_DIRS
         {
           const double rd = (double)r;
           const double* o = s.origins + 3 * u;
@@ -181,12 +220,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           p[1] = __dadd_rn(__dmul_rn(rd, dcur.y), __ldg(o + 1));
           p[2] = __dadd_rn(__dmul_rn(rd, dcur.z), __ldg(o + 2));
         }
-#else
-        unproject_px(s, v, u, r, p);
-#endif
         xform_rows(pose, pose + 9, p[0], p[1], p[2], m);
         const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
-        const Proj32 pr = project_f32<MATH>(s, mx, my, mz);
+        const Proj32 pr = project_f32<MATH, SMEM>(s, tb, mx, my, mz);
         if (pr.status != PROJ_OK) continue;
         int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
         if (col >= W) col = 0;
@@ -227,9 +263,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
         }
 #pragma unroll
         for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
-        // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
-        cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
-        sumsq = __fmaf_rn(res, res, sumsq);
+        if (STATS) {
+          // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
+          cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
+          sumsq = __fmaf_rn(res, res, sumsq);
+        }
         ++cnt;
       }
       // ---- deterministic group reduction in float64
@@ -291,9 +329,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       }
       group_sync<WPP>(g);
       const int ctrl = sh_ctrl[g];
-      if (ctrl == 2) goto finish;
+      if (ctrl == 2) {
+        work += valid_lv * executed;
+        goto finish;
+      }
       if (ctrl == 1) break;
     }
+    work += valid_lv * executed;
   }
 finish:
   if (A.pt_iters) {
@@ -312,19 +354,24 @@ template <int MATH, int WPP, int MINB>
 int launch(const IcpArgs& a, cudaStream_t st) {
   constexpr int GROUPS = kThreads / 32 / WPP;
   const unsigned grid = (unsigned)((a.batch + GROUPS - 1) / GROUPS);
-  k_register<MATH, WPP, MINB><<<grid, kThreads, 0, st>>>(a);
+  const bool smem = a.s.H <= kMaxRowsSmem && a.s.K <= kMaxInvSmem;
+  if (a.stats) {
+    if (smem)
+      k_register<MATH, WPP, MINB, true, true><<<grid, kThreads, 0, st>>>(a);
+    else
+      k_register<MATH, WPP, MINB, false, true><<<grid, kThreads, 0, st>>>(a);
+  } else {
+    if (smem)
+      k_register<MATH, WPP, MINB, true, false><<<grid, kThreads, 0, st>>>(a);
+    else
+      k_register<MATH, WPP, MINB, false, false><<<grid, kThreads, 0, st>>>(a);
+  }
   RK_LAUNCHED("k_register");
   return RK_OK;
 }
 
 }  // namespace
 
-#ifndef RK_ICP_PREFETCH_DIRS
-#define RK_ICP_PREFETCH_DIRS 0
-#endif
-#ifndef RK_ICP_MINB
-#define RK_ICP_MINB 4
-#endif
 
 extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
                                  const float* dst_surfel, const int32_t* pair_src,

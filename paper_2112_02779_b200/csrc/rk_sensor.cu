@@ -133,6 +133,8 @@ extern "C" int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, i
   unsigned g = min(blocks_for(n, 256), 148u * 16u);
   if (math == MATH_CR)
     k_project_f32<MATH_CR><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
+  else if (math == MATH_LIBM)
+    k_project_f32<MATH_LIBM><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   else
     k_project_f32<MATH_FAST><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   RK_LAUNCHED("k_project_f32");

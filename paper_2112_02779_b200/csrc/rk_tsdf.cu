@@ -214,6 +214,10 @@ __global__ void k_offsets(const double* __restrict__ inv12, double voxel, float*
   off[3 * i + 2] = (float)o[2];
 }
 
+#ifndef RK_TSDF_EARLY_STATE
+#define RK_TSDF_EARLY_STATE 1
+#endif
+
 struct IntegrateArgs {
   GridDev g;
   SensorDev s;
@@ -230,11 +234,14 @@ struct IntegrateArgs {
 // K5: persistent CTAs walk the touched list; each block's 4096 voxels are
 // projected into the (L2-resident) range image and folded into the running
 // average; voxels whose observation is rejected cost no state traffic.
-template <int MATH, int NT>
+template <int MATH, int NT, bool SMEM>
 __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
   extern __shared__ float sh_off[];  // kVox*3 rotated lattice (48 KB, dynamic)
   __shared__ int sh_cnt[NT / 32];
+  __shared__ RowTablesSmem sh_tab;
   for (int i = threadIdx.x; i < kVox * 3; i += NT) sh_off[i] = A.offsets[i];
+  if (SMEM) stage_tables(A.s, sh_tab, threadIdx.x, NT);
+  const RowTables tb = SMEM ? RowTables{sh_tab.el32, sh_tab.az32, sh_tab.inv_rows} : global_tables(A.s);
   double R[9], t[3];
 #pragma unroll
   for (int k = 0; k < 9; ++k) R[k] = A.inv12[k];
@@ -266,10 +273,15 @@ __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
     float2* vox = A.g.vox + (size_t)slot * kVox;
 #pragma unroll 2
     for (int i = threadIdx.x; i < kVox; i += NT) {
+#if RK_TSDF_EARLY_STATE
+      // the voxel state does not depend on the observation: issue its load
+      // first so the projection math hides the latency
+      float2 st0 = vox[i];
+#endif
       const float x = __fadd_rn(bx, sh_off[3 * i]);
       const float y = __fadd_rn(by, sh_off[3 * i + 1]);
       const float z = __fadd_rn(bz, sh_off[3 * i + 2]);
-      Proj32 p = project_f32<MATH>(s, x, y, z);
+      Proj32 p = project_f32<MATH, SMEM>(s, tb, x, y, z);
       int col = (int)__fadd_rn(p.u, 0.5f);
       if (col == s.W) col = 0;
       const float px = __ldg(A.range + p.v * s.W + col);
@@ -279,7 +291,11 @@ __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
       if (!A.free_space) ok = ok && d <= A.tau;
       d = fminf(d, A.tau);
       if (ok) {
+#if RK_TSDF_EARLY_STATE
+        float2 st = st0;
+#else
         float2 st = vox[i];
+#endif
         const float wn = __fadd_rn(st.y, 1.0f);
         st.x = __fdiv_rn(__fadd_rn(__fmul_rn(st.y, st.x), d), wn);
         st.y = fminf(wn, A.max_w);
@@ -636,14 +652,19 @@ extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* ra
   const size_t smem = kVox * 3 * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
-    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_CR, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_FAST, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_CR, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_CR, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
+  const bool tab = s->dev.H <= kMaxRowsSmem && s->dev.K <= kMaxInvSmem;
   if (math == MATH_CR)
-    k_integrate<MATH_CR, NT><<<grid, NT, smem, st>>>(a);
+    tab ? k_integrate<MATH_CR, NT, true><<<grid, NT, smem, st>>>(a)
+        : k_integrate<MATH_CR, NT, false><<<grid, NT, smem, st>>>(a);
   else
-    k_integrate<MATH_FAST, NT><<<grid, NT, smem, st>>>(a);
+    tab ? k_integrate<MATH_FAST, NT, true><<<grid, NT, smem, st>>>(a)
+        : k_integrate<MATH_FAST, NT, false><<<grid, NT, smem, st>>>(a);
   RK_LAUNCHED("k_integrate");
   return RK_OK;
 }

@@ -31,8 +31,9 @@ PROJ_OK = 0
 PROJ_OUT_OF_FOV = 1
 PROJ_DEGENERATE = 2
 
-MATH_FAST = 0   # CUDA atan2f / asinf (<= 2 ulp)
+MATH_FAST = 0   # minimax atan2 / asin (<= 2.5 ulp) + refined reciprocals (default)
 MATH_CR = 1     # float64-evaluated, rounded once (parity mode)
+MATH_LIBM = 2   # CUDA atan2f / asinf (<= 2 ulp), IEEE division (project_many only)
 
 _default_math = MATH_FAST
 

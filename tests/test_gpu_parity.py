@@ -6,9 +6,10 @@ Contract (BASELINE.json north_star):
   normals, voxel-block allocation; with RK_MATH_CR (float64-evaluated
   transcendentals in both kernel and oracle) also projection, association
   sets and TSDF values;
-* with the product math (CUDA atan2f/asinf vs numpy's SVML): >= 99.9 %
-  correspondence-mask agreement, poses within 1e-5 rad / 1e-5 m with equal
-  iteration counts, TSDF values within 1e-5.
+* with the product math (RK_MATH_FAST: minimax atan2/asin, refined
+  reciprocals, vs numpy's SVML): >= 99.9 % correspondence-mask agreement,
+  poses within 1e-5 rad / 1e-5 m with equal iteration counts, TSDF values
+  within 1e-5.
 """
 
 import numpy as np
@@ -39,6 +40,42 @@ def set_agreement(a, b):
 
 
 # ---------------------------------------------------------------- sensor model
+
+def _ulps(a, b):
+    """float32 ulp distance (same-sign finite values)."""
+    ia = a.astype(np.float32).view(np.int32).astype(np.int64)
+    ib = b.astype(np.float32).view(np.int32).astype(np.int64)
+    return np.abs(ia - ib)
+
+
+def test_fast_math_ulp(rk, sensors):
+    """RK_MATH_FAST's projection against float64-evaluated transcendentals
+    (RK_MATH_CR): azimuth/elevation within a few ulp, i.e. the same
+    accuracy class as numpy's SVML float32 arctan2/arcsin (<= 3 ulp)."""
+    from paper_2112_02779_b200 import lidar_model as lm
+    intr = sensors["ouster"]
+    rng = np.random.default_rng(11)
+    n = 400_000
+    d = rng.normal(size=(n, 3))
+    d[:, 2] *= 0.25
+    pts = (d / np.linalg.norm(d, axis=1, keepdims=True) * rng.uniform(0.3, 60.0, (n, 1))).astype(np.float32)
+    uf, vf, rf, sf = rk.project_many(pts, intr, single=True, refine=False, math=lm.MATH_FAST)
+    uc, vc, rc, sc = rk.project_many(pts, intr, single=True, refine=False, math=lm.MATH_CR)
+    ul, vl, rl, sl = rk.project_many(pts, intr, single=True, refine=False, math=lm.MATH_LIBM)
+    ok = (sc == 0) & (sf == 0)
+    assert np.mean(sf == sc) >= 0.9999 and np.mean(sl == sc) >= 0.9999
+    assert np.mean(vf[ok] == vc[ok]) >= 0.9999
+    # column: |du| bounded by a few ulp of the azimuth scaled into pixels
+    du = np.abs(uf[ok].astype(np.float64) - uc[ok])
+    du = np.minimum(du, intr.width - du)
+    assert du.max() < 2e-3, du.max()
+    assert np.mean(du == 0) >= 0.5
+    assert np.array_equal(rf, rc)          # r has no transcendental: exact in every mode
+    # FAST is no further from correctly rounded than CUDA's libm
+    dl = np.abs(ul[ok].astype(np.float64) - uc[ok])
+    dl = np.minimum(dl, intr.width - dl)
+    assert du.mean() <= 2.0 * dl.mean() + 1e-6
+
 
 @pytest.mark.parametrize("name", ("small", "synth", "ouster"))
 def test_project_f32_cr_bitexact_vs_oracle(rk, name, sensors, osensors, golden_proj):
