@@ -28,6 +28,9 @@ using namespace rk;
 #ifndef RK_ICP_PREFETCH_DIRS
 #define RK_ICP_PREFETCH_DIRS 1
 #endif
+#ifndef RK_ICP_PIPE
+#define RK_ICP_PIPE 0
+#endif
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
@@ -89,6 +92,53 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
+}
+
+// association tail + point-to-plane terms of one correspondence
+// (registration.py:168-183, 339-352): gate on the stored target, residual,
+// Jacobian, pseudo-Huber IRLS weight, 27 float32 accumulations.
+template <bool STATS>
+__device__ __forceinline__ void accumulate_point(float mx, float my, float mz, const float4& n,
+                                                 const float4& d, const float4& o, float gate2,
+                                                 float inv_k, float* acc, float& cost, float& sumsq,
+                                                 int& cnt) {
+  if (!(n.w > 0.0f)) return;  // stored range > 0 and normal valid
+  const float qx = __fadd_rn(__fmul_rn(n.w, d.x), o.x);
+  const float qy = __fadd_rn(__fmul_rn(n.w, d.y), o.y);
+  const float qz = __fadd_rn(__fmul_rn(n.w, d.z), o.z);
+  const float dx = __fsub_rn(mx, qx), dy = __fsub_rn(my, qy), dz = __fsub_rn(mz, qz);
+  const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+  if (!(d2 <= gate2)) return;
+  // ---- residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352).
+  // Only the reduced sums matter here (pose tolerance 1e-5), so the
+  // weight uses the fast reciprocal square root.
+  const float res = __fadd_rn(__fadd_rn(__fmul_rn(n.x, dx), __fmul_rn(n.y, dy)), __fmul_rn(n.z, dz));
+  float J[6];
+  J[0] = __fsub_rn(__fmul_rn(my, n.z), __fmul_rn(mz, n.y));
+  J[1] = __fsub_rn(__fmul_rn(mz, n.x), __fmul_rn(mx, n.z));
+  J[2] = __fsub_rn(__fmul_rn(mx, n.y), __fmul_rn(my, n.x));
+  J[3] = n.x;
+  J[4] = n.y;
+  J[5] = n.z;
+  const float e = res * inv_k;
+  const float s1 = __fmaf_rn(e, e, 1.0f);
+  const float w = rsqrtf(s1);
+  const float rw = -res * w;
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const float jw = J[i] * w;
+#pragma unroll
+    for (int j = i; j < 6; ++j) { acc[q] = __fmaf_rn(jw, J[j], acc[q]); ++q; }
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
+  if (STATS) {
+    // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
+    cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
+    sumsq = __fmaf_rn(res, res, sumsq);
+  }
+  ++cnt;
 }
 
 template <int WPP>
@@ -177,6 +227,56 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       float cost = 0.0f, sumsq = 0.0f;
       int cnt = 0;
       int off = off0, ui = ui0;
+#if RK_ICP_PIPE
+      // Software-pipelined walk: each trip (1) issues the pose-independent
+      // loads of point k (range, ray, receiver origin), (2) finishes point k-1
+      // whose destination gathers were issued one trip earlier, (3) projects
+      // point k and issues its gathers.  Both dependent-load latencies are
+      // covered by a whole point's arithmetic, without prefetch registers.
+      bool pend = false;
+      float pmx = 0.f, pmy = 0.f, pmz = 0.f;
+      float4 pn = make_float4(0.f, 0.f, 0.f, 0.f), pd = pn, po = pn;
+      for (int k = gtid; k < npix + GT; k += GT) {
+        const bool has = k < npix;
+        float r = 0.0f;
+        double3 dcur = make_double3(0.0, 0.0, 0.0), ocur = dcur;
+        if (has) {
+          const int u = ui * stride;
+          r = __ldg(src + off);
+          const double* dp = s.dirs + 3 * (size_t)off;
+          dcur = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+          const double* op = s.origins + 3 * u;
+          ocur = make_double3(__ldg(op), __ldg(op + 1), __ldg(op + 2));
+          off += step_off;
+          ui += du;
+          if (ui >= Ws) { ui -= Ws; off += wrap_off; }
+        }
+        if (pend) accumulate_point<STATS>(pmx, pmy, pmz, pn, pd, po, gate2, inv_k, acc, cost, sumsq, cnt);
+        pend = false;
+        if (has && range_ok(r, cmin, cmax)) {
+          // ---- association (registration.py:145-183), bit-exact float32/float64 restatement
+          const double rd = (double)r;
+          double m[3];
+          xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
+                     __dadd_rn(__dmul_rn(rd, dcur.y), ocur.y), __dadd_rn(__dmul_rn(rd, dcur.z), ocur.z), m);
+          pmx = (float)m[0];
+          pmy = (float)m[1];
+          pmz = (float)m[2];
+          const Proj32 pr = project_f32<MATH, SMEM>(s, tb, pmx, pmy, pmz);
+          int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
+          if (col >= W) col = 0;
+          const int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
+          // rows rounding to >= H are dropped, not clamped (registration.py:157-159)
+          if (pr.status == PROJ_OK && row < H) {
+            const int flat = row * W + col;
+            pn = __ldg(surf + flat);
+            pd = __ldg(s.dirs32 + flat);
+            po = __ldg(s.origins32 + col);
+            pend = true;
+          }
+        }
+      }
+#else
       // the next point's range (and, with RK_ICP_PREFETCH_DIRS, its ray) is
       // pose-independent: fetched one point ahead so the latency overlaps the
       // current point's math
@@ -232,44 +332,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
         const float4 n = __ldg(surf + flat);
         const float4 d = __ldg(s.dirs32 + flat);
         const float4 o = __ldg(s.origins32 + col);
-        if (!(n.w > 0.0f)) continue;  // stored range > 0 and normal valid
-        const float qx = __fadd_rn(__fmul_rn(n.w, d.x), o.x);
-        const float qy = __fadd_rn(__fmul_rn(n.w, d.y), o.y);
-        const float qz = __fadd_rn(__fmul_rn(n.w, d.z), o.z);
-        const float dx = __fsub_rn(mx, qx), dy = __fsub_rn(my, qy), dz = __fsub_rn(mz, qz);
-        const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-        if (!(d2 <= gate2)) continue;
-        // ---- residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352).
-        // Only the reduced sums matter here (pose tolerance 1e-5), so the
-        // weight uses the fast reciprocal square root.
-        const float res = __fadd_rn(__fadd_rn(__fmul_rn(n.x, dx), __fmul_rn(n.y, dy)), __fmul_rn(n.z, dz));
-        float J[6];
-        J[0] = __fsub_rn(__fmul_rn(my, n.z), __fmul_rn(mz, n.y));
-        J[1] = __fsub_rn(__fmul_rn(mz, n.x), __fmul_rn(mx, n.z));
-        J[2] = __fsub_rn(__fmul_rn(mx, n.y), __fmul_rn(my, n.x));
-        J[3] = n.x;
-        J[4] = n.y;
-        J[5] = n.z;
-        const float e = res * inv_k;
-        const float s1 = __fmaf_rn(e, e, 1.0f);
-        const float w = rsqrtf(s1);
-        const float rw = -res * w;
-        int q = 0;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const float jw = J[i] * w;
-#pragma unroll
-          for (int j = i; j < 6; ++j) { acc[q] = __fmaf_rn(jw, J[j], acc[q]); ++q; }
-        }
-#pragma unroll
-        for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
-        if (STATS) {
-          // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
-          cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
-          sumsq = __fmaf_rn(res, res, sumsq);
-        }
-        ++cnt;
+        accumulate_point<STATS>(mx, my, mz, n, d, o, gate2, inv_k, acc, cost, sumsq, cnt);
       }
+#endif
       // ---- deterministic group reduction in float64
       double* tot = sh_tot[g];
       if (WPP == 1) {

@@ -30,6 +30,9 @@ struct Counters {
   int n_fresh;
   int overflow;
   int n_points;                        // activation input size (gemv quirk)
+  int frame;                           // activation stamp (device-side: graph-replay safe)
+  int work;                            // k_integrate's dynamic block counter
+  int done;                            // k_integrate's finished-CTA ticket
 };
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(long long x, long long y, long long z) {
@@ -132,51 +135,122 @@ __device__ __forceinline__ void touch_point(const GridDev& g, int frame, const d
       for (long long z = lo[2]; z <= hi[2]; ++z) touch_key(g, frame, x, y, z);
 }
 
-__global__ void k_reset_frame(Counters* c) {
+__device__ __forceinline__ void reset_frame(Counters* c) {
+  c->frame += 1;
   c->n_touched = 0;
   c->n_fresh = 0;
   c->max_touched_key = 0ull;
-  c->n_points = 0;
+}
+__global__ void k_reset_frame(Counters* c) { reset_frame(c); }
+
+// touch_point for a whole warp.  A warp is 32 neighbouring pixels of one
+// row, so its cubes share few block keys: lanes elect one lane per distinct
+// key (__match_any_sync) into a per-warp list in shared memory, then the warp
+// resolves the list's keys in parallel -- one round of dependent hash/stamp
+// atomics per warp instead of up to 8 per point.  Every lane must call it;
+// `list` holds 32 * max-keys-per-point entries.
+constexpr int kMaxKeysPerPoint = 8;
+__device__ __forceinline__ void touch_point_warp(const GridDev& g, int frame, const double p[3],
+                                                 bool valid, double radius, double ext,
+                                                 unsigned long long* list) {
+  long long lo[3] = {0, 0, 0};
+  int n[3] = {0, 0, 0};
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = (long long)floor(__ddiv_rn(__dsub_rn(p[c], radius), ext));
+      const long long hi = (long long)floor(__ddiv_rn(__dadd_rn(p[c], radius), ext));
+      n[c] = (int)(hi - lo[c] + 1);
+    }
+  }
+  const int total = n[0] * n[1] * n[2];
+  const int lane = threadIdx.x & 31;
+  const int rounds = __reduce_max_sync(0xffffffffu, total);
+  int n_list = 0;
+  for (int j = 0; j < rounds; ++j) {
+    unsigned long long key = kEmpty;
+    if (j < total) {
+      const int iz = j % n[2], iy = (j / n[2]) % n[1], ix = j / (n[2] * n[1]);
+      key = pack_key(lo[0] + ix, lo[1] + iy, lo[2] + iz);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const bool lead = key != kEmpty && lane == __ffs(peers) - 1;
+    const unsigned leaders = __ballot_sync(0xffffffffu, lead);
+    if (lead && n_list + __popc(leaders & ((1u << lane) - 1u)) < 32 * kMaxKeysPerPoint)
+      list[n_list + __popc(leaders & ((1u << lane) - 1u))] = key;
+    n_list = min(n_list + __popc(leaders), 32 * kMaxKeysPerPoint);
+    if (n_list == 32 * kMaxKeysPerPoint || j + 1 == rounds) {  // flush (duplicates across rounds are harmless)
+      __syncwarp();
+      for (int t = lane; t < n_list; t += 32) {
+        int x, y, z;
+        unpack_key(list[t], x, y, z);
+        touch_key(g, frame, x, y, z);
+      }
+      __syncwarp();
+      n_list = 0;
+    }
+  }
 }
 
-__global__ void k_activate_points(GridDev g, int frame, const double* __restrict__ pts, int64_t n,
+__global__ void k_activate_points(GridDev g, const double* __restrict__ pts, int64_t n,
                                   double radius, double ext) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int frame = g.ctr->frame;
   double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
   touch_point(g, frame, p, radius, ext);
 }
 
-__global__ void k_count_valid(const float* __restrict__ range, int n, float cmin, float cmax,
-                              Counters* c) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int ok = (i < n) && range_ok(range[i], cmin, cmax);
-  ok = __reduce_add_sync(0xffffffffu, ok);
-  if ((threadIdx.x & 31) == 0 && ok) atomicAdd(&c->n_points, ok);
+// open a new frame (stamp, counters; CTA 0) and count the frame's valid
+// pixels (to_point_cloud size, needed for the single-row gemv quirk) into
+// n_points, which the previous k_assign_slots left at zero
+constexpr int kBeginThreads = 256, kBeginCtas = 64;
+__global__ void __launch_bounds__(kBeginThreads) k_begin_image_frame(const float* __restrict__ range, int n,
+                                                                      float cmin, float cmax, Counters* c) {
+  __shared__ int part[kBeginThreads / 32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) reset_frame(c);
+  int cnt = 0;
+  for (int i = blockIdx.x * kBeginThreads + threadIdx.x; i < n; i += kBeginThreads * gridDim.x)
+    cnt += range_ok(__ldg(range + i), cmin, cmax) ? 1 : 0;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kBeginThreads / 32; ++w) tot += part[w];
+    if (tot) atomicAdd(&c->n_points, tot);
+  }
 }
 
 // to_point_cloud -> pose.apply -> activate_blocks, fused (sdf_volume.py:198-208)
-__global__ void k_activate_image(GridDev g, SensorDev s, int frame, const float* __restrict__ range,
+__global__ void __launch_bounds__(256) k_activate_image(GridDev g, SensorDev s, const float* __restrict__ range,
                                  const double* __restrict__ pose12, double radius, double ext,
                                  float cmin, float cmax) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= s.H * s.W) return;
-  float r = range[i];
-  if (!range_ok(r, cmin, cmax)) return;
-  double pose[12];
+  __shared__ unsigned long long keys[256 / 32][32 * kMaxKeysPerPoint];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // whole warps stay (warp dedup)
+  const int frame = g.ctr->frame;
+  const bool in = i < s.H * s.W;
+  const float r = in ? range[i] : 0.0f;
+  const bool valid = in && range_ok(r, cmin, cmax);
+  double w[3] = {0.0, 0.0, 0.0};
+  if (valid) {
+    double pose[12];
 #pragma unroll
-  for (int k = 0; k < 12; ++k) pose[k] = pose12[k];
-  double p[3], w[3];
-  unproject_px(s, i / s.W, i % s.W, r, p);
-  xform_rows(pose, pose + 9, p[0], p[1], p[2], w, g.ctr->n_points == 1);
-  touch_point(g, frame, w, radius, ext);
+    for (int k = 0; k < 12; ++k) pose[k] = pose12[k];
+    double p[3];
+    unproject_px(s, i / s.W, i % s.W, r, p);
+    xform_rows(pose, pose + 9, p[0], p[1], p[2], w, g.ctr->n_points == 1);
+  }
+  touch_point_warp(g, frame, w, valid, radius, ext, keys[threadIdx.x >> 5]);
 }
 
-// fresh keys -> pool slots (deterministic per key; slot order follows the list)
-__global__ void k_assign_slots(GridDev g) {
+// fresh keys -> pool slots (slot order follows the fresh list); one CTA,
+// which then publishes the new block count
+constexpr int kAssignThreads = 1024;
+__global__ void __launch_bounds__(kAssignThreads) k_assign_slots(GridDev g) {
   const int nf = g.ctr->n_fresh;
   const long long base = g.ctr->n_blocks;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+  for (int i = threadIdx.x; i < nf; i += kAssignThreads) {
     int h = g.fresh[i];
     long long slot = base + i;
     if (slot < g.cap_blocks) {
@@ -189,29 +263,13 @@ __global__ void k_assign_slots(GridDev g) {
       atomicExch(&g.ctr->overflow, 1);
     }
   }
-}
-
-__global__ void k_finish_slots(GridDev g) {
-  long long nb = g.ctr->n_blocks + g.ctr->n_fresh;
-  g.ctr->n_blocks = nb < g.cap_blocks ? nb : g.cap_blocks;
-  g.ctr->n_fresh = 0;
-}
-
-// rotated voxel-centre lattice of one block, float32 (sdf_volume.py:160)
-__global__ void k_offsets(const double* __restrict__ inv12, double voxel, float* off) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= kVox) return;
-  double R[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) R[k] = inv12[k];
-  double l0 = __dmul_rn(__dadd_rn((double)(i >> 8), 0.5), voxel);
-  double l1 = __dmul_rn(__dadd_rn((double)((i >> 4) & 15), 0.5), voxel);
-  double l2 = __dmul_rn(__dadd_rn((double)(i & 15), 0.5), voxel);
-  double o[3];
-  xform_rows(R, nullptr, l0, l1, l2, o);
-  off[3 * i] = (float)o[0];
-  off[3 * i + 1] = (float)o[1];
-  off[3 * i + 2] = (float)o[2];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long nb = base + nf;
+    g.ctr->n_blocks = nb < g.cap_blocks ? nb : g.cap_blocks;
+    g.ctr->n_fresh = 0;
+    g.ctr->n_points = 0;  // k_begin_image_frame of the next frame accumulates into it
+  }
 }
 
 #ifndef RK_TSDF_EARLY_STATE
@@ -223,7 +281,7 @@ struct IntegrateArgs {
   SensorDev s;
   const float* range;
   const double* inv12;
-  const float* offsets;
+  double voxel;
   double block_ext;  // 16 * voxel_size
   float tau, max_w, cmin, cmax;
   int free_space;
@@ -231,15 +289,19 @@ struct IntegrateArgs {
   const long long* global_touch;  // sharded grids: {frame key count, max key} over all ranks
 };
 
-// K5: persistent CTAs walk the touched list; each block's 4096 voxels are
-// projected into the (L2-resident) range image and folded into the running
-// average; voxels whose observation is rejected cost no state traffic.
+// K5: persistent CTAs (kIntegrateCtasPerSm per SM) pull touched blocks from
+// a device counter; each block's 4096 voxels are projected into the
+// (L2-resident) range image and folded into the running average; voxels whose
+// observation is rejected cost no state traffic.  Every CTA first builds the
+// frame's rotated voxel-centre lattice in shared memory (sdf_volume.py:160:
+// f32(((local + 0.5) * voxel) @ inv.R^T), the OpenBLAS FMA order) -- 36
+// float64 ops per thread instead of a separate launch and a 48 KB copy.
 template <int MATH, int NT, bool SMEM>
-__global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
+__global__ void __launch_bounds__(NT, 1024 / NT) k_integrate(IntegrateArgs A) {
   extern __shared__ float sh_off[];  // kVox*3 rotated lattice (48 KB, dynamic)
   __shared__ int sh_cnt[NT / 32];
+  __shared__ int sh_e;
   __shared__ RowTablesSmem sh_tab;
-  for (int i = threadIdx.x; i < kVox * 3; i += NT) sh_off[i] = A.offsets[i];
   if (SMEM) stage_tables(A.s, sh_tab, threadIdx.x, NT);
   const RowTables tb = SMEM ? RowTables{sh_tab.el32, sh_tab.az32, sh_tab.inv_rows} : global_tables(A.s);
   double R[9], t[3];
@@ -247,6 +309,16 @@ __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
   for (int k = 0; k < 9; ++k) R[k] = A.inv12[k];
 #pragma unroll
   for (int k = 0; k < 3; ++k) t[k] = A.inv12[9 + k];
+  for (int i = threadIdx.x; i < kVox; i += NT) {
+    const double l0 = __dmul_rn(__dadd_rn((double)(i >> 8), 0.5), A.voxel);
+    const double l1 = __dmul_rn(__dadd_rn((double)((i >> 4) & 15), 0.5), A.voxel);
+    const double l2 = __dmul_rn(__dadd_rn((double)(i & 15), 0.5), A.voxel);
+    double o[3];
+    xform_rows(R, nullptr, l0, l1, l2, o);
+    sh_off[3 * i] = (float)o[0];
+    sh_off[3 * i + 1] = (float)o[1];
+    sh_off[3 * i + 2] = (float)o[2];
+  }
   __syncthreads();
   const SensorDev& s = A.s;
   const int n_touched = A.g.ctr->n_touched;
@@ -259,7 +331,12 @@ __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
       A.global_touch ? (unsigned long long)A.global_touch[1] : A.g.ctr->max_touched_key;
   const bool lone_tail = (n_all % kChunkBlocks) == 1;
   int count = 0;
-  for (int e = blockIdx.x; e < n_touched; e += gridDim.x) {
+  for (;;) {
+    if (threadIdx.x == 0) sh_e = atomicAdd(&A.g.ctr->work, 1);
+    __syncthreads();
+    const int e = sh_e;
+    __syncthreads();  // sh_e is rewritten by the next fetch
+    if (e >= n_touched) break;
     const int h = A.g.touched[e];
     const int slot = A.g.h_slot[h];
     if (slot < 0) continue;
@@ -307,16 +384,26 @@ __global__ void __launch_bounds__(NT) k_integrate(IntegrateArgs A) {
   count = __reduce_add_sync(0xffffffffu, count);
   if ((threadIdx.x & 31) == 0) sh_cnt[threadIdx.x >> 5] = count;
   __syncthreads();
-  if (threadIdx.x == 0 && A.updated) {
-    long long tot = 0;
-    for (int w = 0; w < NT / 32; ++w) tot += sh_cnt[w];
-    if (tot) atomicAdd((unsigned long long*)A.updated, (unsigned long long)tot);
+  if (threadIdx.x == 0) {
+    if (A.updated) {
+      long long tot = 0;
+      for (int w = 0; w < NT / 32; ++w) tot += sh_cnt[w];
+      if (tot) atomicAdd((unsigned long long*)A.updated, (unsigned long long)tot);
+    }
+    // the last CTA out rewinds the block counter for the next launch (every
+    // CTA has stopped fetching once it takes its ticket)
+    __threadfence();
+    if (atomicAdd(&A.g.ctr->done, 1) == (int)gridDim.x - 1) {
+      A.g.ctr->work = 0;
+      A.g.ctr->done = 0;
+    }
   }
 }
 
-__global__ void k_set_touched(GridDev g, int frame, const int32_t* __restrict__ keys, int64_t n) {
+__global__ void k_set_touched(GridDev g, const int32_t* __restrict__ keys, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int frame = g.ctr->frame;
   // explicit frame_keys: they need not exist yet (integrate() on unknown keys
   // raises KeyError in the reference; here they are simply skipped)
   unsigned long long key = pack_key(keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
@@ -448,14 +535,41 @@ __global__ void k_rehash(GridDev g, long long nb) {
 }  // namespace
 
 // ------------------------------------------------------------------ host side
+#ifndef RK_TSDF_THREADS
+#define RK_TSDF_THREADS 512
+#endif
+constexpr int kIntegrateThreads = RK_TSDF_THREADS;
+constexpr int kIntegrateCtasPerSm = 1024 / kIntegrateThreads;  // 64 registers x 1024 threads per SM
+constexpr size_t kLatticeBytes = kVox * 3 * sizeof(float);
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static cudaError_t set_integrate_attrs() {
+  constexpr int NT = kIntegrateThreads;
+  (void)num_sms();  // cached now: rk_grid_integrate may later run under graph capture
+  const int smem = (int)kLatticeBytes;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_integrate<MATH_CR, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_integrate<MATH_CR, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  return cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
 struct rk_grid {
   double voxel, trunc;
   float max_weight;
   int free_space;
-  int frame;
   GridDev d;
   unsigned long long hash_cap;
-  float* offsets;  // 4096*3
   const long long* global_touch = nullptr;  // device {count, max key} (sharded grids)
 };
 
@@ -524,7 +638,6 @@ extern "C" int rk_grid_create(double voxel_size, double truncation, float max_we
   g->trunc = truncation;
   g->max_weight = max_weight;
   g->free_space = free_space;
-  g->frame = 1;
   g->d.shard_rank = 0;
   g->d.shard_world = 1;
   if (capacity_blocks < 64) capacity_blocks = 64;
@@ -532,7 +645,7 @@ extern "C" int rk_grid_create(double voxel_size, double truncation, float max_we
   if (rc) { delete g; return rc; }
   RK_CUDA(cudaMalloc(&g->d.ctr, sizeof(Counters)));
   RK_CUDA(cudaMemset(g->d.ctr, 0, sizeof(Counters)));
-  RK_CUDA(cudaMalloc(&g->offsets, kVox * 3 * sizeof(float)));
+  RK_CUDA(set_integrate_attrs());
   RK_CUDA(cudaDeviceSynchronize());
   *out = g;
   return RK_OK;
@@ -543,7 +656,6 @@ extern "C" int rk_grid_destroy(rk_grid* g) {
   cudaDeviceSynchronize();
   free_tables(g->d);
   cudaFree(g->d.ctr);
-  cudaFree(g->offsets);
   delete g;
   return RK_OK;
 }
@@ -572,7 +684,6 @@ extern "C" int rk_grid_reserve(rk_grid* g, int64_t capacity_blocks, void* stream
   RK_CUDA(cudaMemcpyAsync(g->d.ctr, &c, sizeof(c), cudaMemcpyHostToDevice, st));
   RK_CUDA(cudaStreamSynchronize(st));
   free_tables(old);
-  g->frame += 1;
   return RK_OK;
 }
 
@@ -589,8 +700,7 @@ extern "C" int rk_grid_info(rk_grid* g, int64_t* out4, void* stream) {
 }
 
 static int finish_activation(rk_grid* g, cudaStream_t st) {
-  k_assign_slots<<<64, 256, 0, st>>>(g->d);
-  k_finish_slots<<<1, 1, 0, st>>>(g->d);
+  k_assign_slots<<<1, kAssignThreads, 0, st>>>(g->d);
   RK_LAUNCHED("rk_grid activation");
   return RK_OK;
 }
@@ -598,10 +708,9 @@ static int finish_activation(rk_grid* g, cudaStream_t st) {
 extern "C" int rk_grid_activate_points(rk_grid* g, const double* pts, int64_t n, double radius,
                                        void* stream) {
   cudaStream_t st = S(stream);
-  g->frame += 1;
   k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
   if (n > 0)
-    k_activate_points<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, g->frame, pts, n, radius,
+    k_activate_points<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, pts, n, radius,
                                                                     kEdge * g->voxel);
   return finish_activation(g, st);
 }
@@ -610,20 +719,17 @@ extern "C" int rk_grid_activate_image(rk_grid* g, const rk_sensor* s, const floa
                                       const double* pose12, double radius, float clip_min,
                                       float clip_max, void* stream) {
   cudaStream_t st = S(stream);
-  g->frame += 1;
   const int n = s->dev.H * s->dev.W;
-  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
-  k_count_valid<<<(n + 255) / 256, 256, 0, st>>>(range, n, clip_min, clip_max, g->d.ctr);
-  k_activate_image<<<(n + 255) / 256, 256, 0, st>>>(g->d, s->dev, g->frame, range, pose12, radius,
+  k_begin_image_frame<<<kBeginCtas, kBeginThreads, 0, st>>>(range, n, clip_min, clip_max, g->d.ctr);
+  k_activate_image<<<(n + 255) / 256, 256, 0, st>>>(g->d, s->dev, range, pose12, radius,
                                                     kEdge * g->voxel, clip_min, clip_max);
   return finish_activation(g, st);
 }
 
 extern "C" int rk_grid_set_touched(rk_grid* g, const int32_t* keys, int64_t n, void* stream) {
   cudaStream_t st = S(stream);
-  g->frame += 1;
   k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
-  if (n > 0) k_set_touched<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, g->frame, keys, n);
+  if (n > 0) k_set_touched<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, keys, n);
   RK_LAUNCHED("k_set_touched");
   return RK_OK;
 }
@@ -632,13 +738,12 @@ extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* ra
                                  const double* inv12, float clip_min, float clip_max, int math,
                                  int64_t* updated, void* stream) {
   cudaStream_t st = S(stream);
-  k_offsets<<<kVox / 256, 256, 0, st>>>(inv12, g->voxel, g->offsets);
   IntegrateArgs a;
   a.g = g->d;
   a.s = s->dev;
   a.range = range;
   a.inv12 = inv12;
-  a.offsets = g->offsets;
+  a.voxel = g->voxel;
   a.block_ext = kEdge * g->voxel;
   a.tau = (float)g->trunc;
   a.max_w = g->max_weight;
@@ -647,17 +752,9 @@ extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* ra
   a.free_space = g->free_space;
   a.updated = reinterpret_cast<long long*>(updated);
   a.global_touch = g->global_touch;
-  constexpr int NT = 256;
-  const unsigned grid = 148 * 4;
-  const size_t smem = kVox * 3 * sizeof(float);
-  static bool attr_set = false;
-  if (!attr_set) {
-    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_CR, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_CR, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    RK_CUDA(cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  constexpr int NT = kIntegrateThreads;
+  const unsigned grid = (unsigned)(num_sms() * kIntegrateCtasPerSm);
+  const size_t smem = kLatticeBytes;
   const bool tab = s->dev.H <= kMaxRowsSmem && s->dev.K <= kMaxInvSmem;
   if (math == MATH_CR)
     tab ? k_integrate<MATH_CR, NT, true><<<grid, NT, smem, st>>>(a)
@@ -757,7 +854,6 @@ extern "C" int rk_grid_clear(rk_grid* g, void* stream) {
   RK_CUDA(cudaMemsetAsync(g->d.h_slot, 0xff, g->hash_cap * sizeof(int32_t), st));
   k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr);
   RK_LAUNCHED("rk_grid_clear");
-  g->frame += 1;
   return RK_OK;
 }
 

@@ -212,6 +212,7 @@ class VoxelBlockGrid:
             raise ValueError("truncation must be > 0")
         self._handle = None
         self._lib = None
+        self._graphs = {}   # CUDA graphs recorded against this grid's tables (pipeline.py)
         self.blocks = _DeviceBlocks(self)
 
     # -- device handle
@@ -246,6 +247,7 @@ class VoxelBlockGrid:
         if capacity > self.capacity:
             nat.call("rk_grid_reserve", self._handle, int(capacity), nat.stream_ptr())
             self.capacity = int(capacity)
+            self._graphs.clear()   # recorded launches point at the old tables
             self.blocks._bump()
 
     def _ensure_capacity(self, n):

@@ -398,6 +398,33 @@ def test_tsdf_street_frame_vs_reference(rk, sensors, golden_tsdf, golden_icp):
         assert np.mean(np.abs(b.tsdf.reshape(-1) - ref[:, 0]) <= 1e-5) >= 0.999
 
 
+def test_integrate_sequence_graph_replay_matches_eager(rk, sensors, golden_icp):
+    """pipeline.integrate_sequence(graph=True): the recorded launches replayed
+    on a cleared grid reproduce the eager sequence bit for bit (frame stamps
+    and block counters live on the device)."""
+    import torch
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = sensors["ouster"]
+    traj = scenes.street_trajectory(6, seed=0)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    poses = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    inv = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).cuda()
+    out = []
+    upd = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for graph in (False, True, True):
+        grid = rk.VoxelBlockGrid(voxel_size=0.05, capacity=8192) if not out else out_grid
+        pipeline.clear_grid(grid)
+        upd.zero_()
+        pipeline.integrate_sequence(grid, intr, frames, poses, inv, clip_max=30.0, updated=upd,
+                                    graph=graph)
+        keys, vox = _grid_vox(grid)
+        out.append((int(upd.item()), keys, vox))
+        out_grid = grid
+    assert len(out_grid._graphs) == 1          # recorded once, replayed once
+    for n, keys, vox in out[1:]:
+        assert n == out[0][0] and keys == out[0][1] and np.array_equal(vox, out[0][2])
+
+
 def test_hash_sharded_grid_equals_single_grid(rk, sensors, golden_icp):
     """Two block shards (emulated in one process) reproduce the unsharded grid
     bit for bit, including the global sorted-chunk arithmetic."""
