@@ -25,12 +25,6 @@ using namespace rk;
 #ifndef RK_ICP_MINB
 #define RK_ICP_MINB 4
 #endif
-#ifndef RK_ICP_PREFETCH_DIRS
-#define RK_ICP_PREFETCH_DIRS 1
-#endif
-#ifndef RK_ICP_PIPE
-#define RK_ICP_PIPE 0
-#endif
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
@@ -141,6 +135,33 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   ++cnt;
 }
 
+// one source point against the destination (registration.py:145-183): the
+// bit-exact float64 unprojection + FMA-chain transform, float32 projection,
+// stride-aligned pixel, then accumulate_point.
+template <int MATH, bool SMEM, bool STATS>
+__device__ __forceinline__ void associate_point(const SensorDev& s, const RowTables& tb,
+                                                const double* pose, float r, const double3& dcur,
+                                                const double3& ocur, const float4* surf, int stride,
+                                                float inv_s, float gate2, float inv_k, float* acc,
+                                                float& cost, float& sumsq, int& cnt) {
+  const double rd = (double)r;
+  double m[3];
+  xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
+             __dadd_rn(__dmul_rn(rd, dcur.y), ocur.y), __dadd_rn(__dmul_rn(rd, dcur.z), ocur.z), m);
+  const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
+  const Proj32 pr = project_f32<MATH, SMEM>(s, tb, mx, my, mz);
+  if (pr.status != PROJ_OK) return;
+  int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
+  if (col >= s.W) col = 0;
+  const int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
+  if (row >= s.H) return;  // dropped, not clamped (registration.py:157-159)
+  const int flat = row * s.W + col;
+  const float4 n = __ldg(surf + flat);
+  const float4 d = __ldg(s.dirs32 + flat);
+  const float4 o = __ldg(s.origins32 + col);
+  accumulate_point<STATS>(mx, my, mz, n, d, o, gate2, inv_k, acc, cost, sumsq, cnt);
+}
+
 template <int WPP>
 __device__ __forceinline__ void group_sync(int g) {
   if (WPP == 1) {
@@ -202,6 +223,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     const int wrap_off = stride * W - Ws * stride;
     const int vi0 = gtid / Ws, ui0 = gtid - vi0 * Ws;
     const int off0 = vi0 * stride * W + ui0 * stride;
+    const bool col_mode = Ws % GT == 0;
+    const int row_step = stride * W;
     // executed work (the roofline's unit) = valid points of this level x the
     // iterations run; counted once per level, outside the hot loop
     unsigned valid_lv = 0;
@@ -226,115 +249,61 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       for (int i = 0; i < 27; ++i) acc[i] = 0.0f;
       float cost = 0.0f, sumsq = 0.0f;
       int cnt = 0;
-      int off = off0, ui = ui0;
-#if RK_ICP_PIPE
-      // Software-pipelined walk: each trip (1) issues the pose-independent
-      // loads of point k (range, ray, receiver origin), (2) finishes point k-1
-      // whose destination gathers were issued one trip earlier, (3) projects
-      // point k and issues its gathers.  Both dependent-load latencies are
-      // covered by a whole point's arithmetic, without prefetch registers.
-      bool pend = false;
-      float pmx = 0.f, pmy = 0.f, pmz = 0.f;
-      float4 pn = make_float4(0.f, 0.f, 0.f, 0.f), pd = pn, po = pn;
-      for (int k = gtid; k < npix + GT; k += GT) {
-        const bool has = k < npix;
-        float r = 0.0f;
-        double3 dcur = make_double3(0.0, 0.0, 0.0), ocur = dcur;
-        if (has) {
-          const int u = ui * stride;
-          r = __ldg(src + off);
+      if (col_mode) {
+        // column-owner walk (Ws % GT == 0): each lane owns view columns
+        // gtid, gtid + GT, ... and walks them down the rows with a constant
+        // pointer step; the receiver origin depends on the column only
+        for (int cj = gtid; cj < Ws; cj += GT) {
+          const int u = cj * stride;
+          const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
+                                            __ldg(s.origins + 3 * u + 2));
+          const float* sp = src + u;
+          const double* dp = s.dirs + 3 * (size_t)u;
+          float r_next = __ldg(sp);
+          double3 d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+          for (int vi = 0; vi < Hs; ++vi) {
+            const float r = r_next;
+            const double3 dcur = d_next;
+            sp += row_step;
+            dp += 3 * (size_t)row_step;
+            if (vi + 1 < Hs) {  // next row's range and ray, one point ahead
+              r_next = __ldg(sp);
+              d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+            }
+            if (!range_ok(r, cmin, cmax)) continue;
+            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, inv_s, gate2,
+                                               inv_k, acc, cost, sumsq, cnt);
+          }
+        }
+      } else {
+        // generic row-major walk of the stride view by GT-point steps
+        int off = off0, ui = ui0;
+        float r_next = 0.0f;
+        double3 d_next = make_double3(0.0, 0.0, 0.0);
+        if (gtid < npix) {
+          r_next = __ldg(src + off);
           const double* dp = s.dirs + 3 * (size_t)off;
-          dcur = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
-          const double* op = s.origins + 3 * u;
-          ocur = make_double3(__ldg(op), __ldg(op + 1), __ldg(op + 2));
+          d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
+        }
+        for (int k = gtid; k < npix; k += GT) {
+          const float r = r_next;
+          const double3 dcur = d_next;
+          const int u = ui * stride;
           off += step_off;
           ui += du;
           if (ui >= Ws) { ui -= Ws; off += wrap_off; }
-        }
-        if (pend) accumulate_point<STATS>(pmx, pmy, pmz, pn, pd, po, gate2, inv_k, acc, cost, sumsq, cnt);
-        pend = false;
-        if (has && range_ok(r, cmin, cmax)) {
-          // ---- association (registration.py:145-183), bit-exact float32/float64 restatement
-          const double rd = (double)r;
-          double m[3];
-          xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
-                     __dadd_rn(__dmul_rn(rd, dcur.y), ocur.y), __dadd_rn(__dmul_rn(rd, dcur.z), ocur.z), m);
-          pmx = (float)m[0];
-          pmy = (float)m[1];
-          pmz = (float)m[2];
-          const Proj32 pr = project_f32<MATH, SMEM>(s, tb, pmx, pmy, pmz);
-          int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
-          if (col >= W) col = 0;
-          const int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
-          // rows rounding to >= H are dropped, not clamped (registration.py:157-159)
-          if (pr.status == PROJ_OK && row < H) {
-            const int flat = row * W + col;
-            pn = __ldg(surf + flat);
-            pd = __ldg(s.dirs32 + flat);
-            po = __ldg(s.origins32 + col);
-            pend = true;
+          if (k + GT < npix) {
+            r_next = __ldg(src + off);
+            const double* dp = s.dirs + 3 * (size_t)off;
+            d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
           }
+          if (!range_ok(r, cmin, cmax)) continue;
+          const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
+                                            __ldg(s.origins + 3 * u + 2));
+          associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, inv_s, gate2,
+                                             inv_k, acc, cost, sumsq, cnt);
         }
       }
-#else
-      // the next point's range (and, with RK_ICP_PREFETCH_DIRS, its ray) is
-      // pose-independent: fetched one point ahead so the latency overlaps the
-      // current point's math
-      float r_next = 0.0f;
-#if RK_ICP_PREFETCH_DIRS
-      double3 d_next = make_double3(0.0, 0.0, 0.0);
-#endif
-      if (gtid < npix) {
-        r_next = __ldg(src + off);
-#if RK_ICP_PREFETCH_DIRS
-        const double* dp = s.dirs + 3 * (size_t)off;
-        d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
-#endif
-      }
-      for (int k = gtid; k < npix; k += GT) {
-        const float r = r_next;
-#if RK_ICP_PREFETCH_DIRS
-        const double3 dcur = d_next;
-#else
-        const double* dcp = s.dirs + 3 * (size_t)off;
-        const double3 dcur = make_double3(__ldg(dcp), __ldg(dcp + 1), __ldg(dcp + 2));
-#endif
-        const int u = ui * stride;
-        off += step_off;
-        ui += du;
-        if (ui >= Ws) { ui -= Ws; off += wrap_off; }
-        if (k + GT < npix) {
-          r_next = __ldg(src + off);
-#if RK_ICP_PREFETCH_DIRS
-          const double* dp = s.dirs + 3 * (size_t)off;
-          d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
-#endif
-        }
-        if (!range_ok(r, cmin, cmax)) continue;
-        // ---- association (registration.py:145-183), bit-exact float32/float64 restatement
-        double p[3], m[3];
-        {
-          const double rd = (double)r;
-          const double* o = s.origins + 3 * u;
-          p[0] = __dadd_rn(__dmul_rn(rd, dcur.x), __ldg(o + 0));
-          p[1] = __dadd_rn(__dmul_rn(rd, dcur.y), __ldg(o + 1));
-          p[2] = __dadd_rn(__dmul_rn(rd, dcur.z), __ldg(o + 2));
-        }
-        xform_rows(pose, pose + 9, p[0], p[1], p[2], m);
-        const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
-        const Proj32 pr = project_f32<MATH, SMEM>(s, tb, mx, my, mz);
-        if (pr.status != PROJ_OK) continue;
-        int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
-        if (col >= W) col = 0;
-        const int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
-        if (row >= H) continue;  // dropped, not clamped (registration.py:157-159)
-        const int flat = row * W + col;
-        const float4 n = __ldg(surf + flat);
-        const float4 d = __ldg(s.dirs32 + flat);
-        const float4 o = __ldg(s.origins32 + col);
-        accumulate_point<STATS>(mx, my, mz, n, d, o, gate2, inv_k, acc, cost, sumsq, cnt);
-      }
-#endif
       // ---- deterministic group reduction in float64
       double* tot = sh_tot[g];
       if (WPP == 1) {
