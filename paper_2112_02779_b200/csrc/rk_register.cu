@@ -19,6 +19,9 @@
 // CTA-wide barrier) remain selectable with RK_ICP_WPP for experiments.
 #include "rk_common.cuh"
 #include "rk_linalg.cuh"
+#if RK_ICP_TIME_SOLVE
+#include <cstdio>
+#endif
 
 using namespace rk;
 
@@ -80,6 +83,115 @@ __device__ __noinline__ int solve_step(const double* tot, int n_corr, double* po
   const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
   const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
   return (nr < rot_eps && nt < trans_eps) ? 1 : 0;
+}
+
+// The per-iteration update (registration.py:266-282) by one warp: the common
+// case -- an SPD system whose condition number the cheap bounds already
+// settle -- runs lane-parallel in registers (right-looking Cholesky with one
+// lower-triangle entry per lane, L^-1 by per-lane column substitution for the
+// trace(H^-1) bound, x = M^T M b), then lane 0 applies the twist.  Anything
+// else (non-positive pivot, a condition number inside the bounds' band) takes
+// the exact serial solve_step.  Returns the warp-uniform control word.
+__device__ __forceinline__ int warp_solve_step(const double* tot, int n_corr, double* pose,
+                                               int min_corr, double rot_eps, double trans_eps,
+                                               int* status) {
+  const int lane = threadIdx.x & 31;
+  if (n_corr < min_corr) {
+    if (lane == 0) *status = RK_ICP_TOO_FEW;
+    return 2;
+  }
+  // lane t < 21 owns lower entry (li, lj), t = li (li + 1) / 2 + lj
+  int li = 0;
+  while ((li + 1) * (li + 2) / 2 <= lane) ++li;
+  const int lj = lane - li * (li + 1) / 2;
+  const bool own = lane < 21;
+  // H[li][lj] = upper entry (lj, li) in tot's row-major upper enumeration
+  const double h0 = own ? tot[lj * (11 - lj) / 2 + li] : 0.0;
+  double a = h0;
+  double pmax = 0.0, pmin = 0.0, dinv[6];
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double d = __shfl_sync(0xffffffffu, a, k * (k + 1) / 2 + k);
+    if (!(d > 0.0)) { ok = false; break; }
+    pmax = k ? fmax(pmax, d) : d;
+    pmin = k ? fmin(pmin, d) : d;
+    const double inv = rsqrt(d);
+    dinv[k] = inv;
+    if (own && lj == k) a = (li == k) ? d * inv : a * inv;
+    const int s1 = own && li > k ? li * (li + 1) / 2 + k : 0;
+    const int s2 = own && lj > k ? lj * (lj + 1) / 2 + k : 0;
+    const double lik = __shfl_sync(0xffffffffu, a, s1);
+    const double ljk = __shfl_sync(0xffffffffu, a, s2);
+    if (own && lj > k) a = __fma_rn(-lik, ljk, a);
+  }
+  if (!ok || pmax > 1e12 * pmin) {
+    // degenerate for sure (pivot ratio bounds cond from below) or not SPD:
+    // the exact serial path decides
+    int ctrl = 0;
+    if (lane == 0) ctrl = solve_step(tot, n_corr, pose, min_corr, rot_eps, trans_eps, status);
+    return __shfl_sync(0xffffffffu, ctrl, 0);
+  }
+  // ||H||_F^2 (off-diagonal entries twice)
+  double fh = own ? (li == lj ? h0 * h0 : 2.0 * h0 * h0) : 0.0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) fh += __shfl_xor_sync(0xffffffffu, fh, off);
+  // column j = lane of M = L^-1: M_jj = dinv_j, M_ij = -dinv_i sum_{k=j}^{i-1} L_ik M_kj
+  double m[6];
+  const int j = lane < 6 ? lane : 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) m[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double acc = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      const double lik = __shfl_sync(0xffffffffu, a, i * (i + 1) / 2 + k);
+      if (k >= j) acc = __fma_rn(-lik, m[k], acc);
+    }
+    m[i] = i >= j ? acc * dinv[i] : 0.0;
+  }
+  double tr = 0.0;
+  if (lane < 6)
+#pragma unroll
+    for (int i = 0; i < 6; ++i) tr = __fma_rn(m[i], m[i], tr);
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, off);
+  if (!(sqrt(fh) * tr <= 1e12)) {  // inside the bounds' band: exact eigenvalues decide
+    int ctrl = 0;
+    if (lane == 0) ctrl = solve_step(tot, n_corr, pose, min_corr, rot_eps, trans_eps, status);
+    return __shfl_sync(0xffffffffu, ctrl, 0);
+  }
+  // x = H^-1 b = M^T (M b): y_i = sum_j M_ij b_j over lanes j < 6
+  const double bj = lane < 6 ? tot[21 + lane] : 0.0;
+  double y[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double v = lane < 6 ? m[i] * bj : 0.0;
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    y[i] = v;
+  }
+  double xj = 0.0;  // lane j: x_j = sum_i M_ij y_i
+#pragma unroll
+  for (int i = 0; i < 6; ++i) xj = __fma_rn(m[i], y[i], xj);
+  double xi[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) xi[i] = __shfl_sync(0xffffffffu, xj, i);
+  int ctrl = 0;
+  if (lane == 0) {
+    double P[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) P[i] = pose[i];
+    se3_left_update(xi, P);
+    if (orth_defect(P) > 1e-12) reorthonormalize(P);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) pose[i] = P[i];
+    const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+    const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+    ctrl = (nr < rot_eps && nt < trans_eps) ? 1 : 0;
+  }
+  return __shfl_sync(0xffffffffu, ctrl, 0);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -202,6 +314,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   __shared__ int sh_ctrl[GROUPS];
   if (gtid < 12) sh_pose[g][gtid] = A.init12[pair * 12 + gtid];
   int n_done = 0, status = RK_ICP_CONVERGED;
+#if RK_ICP_TIME_SOLVE
+  long long t_solve_acc = 0;
+  const long long t_kernel0 = clock64();
+#endif
   unsigned work = 0;  // valid source points visited (all iterations), per thread
   const float cmin = A.cfg.clip_min, cmax = A.cfg.clip_max;
 
@@ -342,24 +458,38 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
       }
       group_sync<WPP>(g);
-      if (gtid == 0) {
+      if (gtid < 32) {  // the group's first warp updates the pose
         const int n_corr = sh_cnt[g * WPP];
         // (cfg fields by value: taking a kernel parameter's address would
         // spill the whole argument block to local memory)
-        const int ctrl = solve_step(tot, n_corr, sh_pose[g], A.cfg.min_corr, A.cfg.rot_eps,
-                                    A.cfg.trans_eps, &status);
-        if (ctrl != 2) {
-          if (A.stats && n_done < A.stats_stride) {
-            double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
-            row[0] = stride;
-            row[1] = it;
-            row[2] = n_corr;
-            row[3] = kern * kern * tot[27];
-            row[4] = sqrt(tot[28] / n_corr);
+#if RK_ICP_TIME_SOLVE
+        const long long t_solve0 = clock64();
+#endif
+#if RK_ICP_SERIAL_SOLVE
+        int ctrl = 0;
+        if (gtid == 0) ctrl = solve_step(tot, n_corr, sh_pose[g], A.cfg.min_corr, A.cfg.rot_eps,
+                                         A.cfg.trans_eps, &status);
+#else
+        const int ctrl = warp_solve_step(tot, n_corr, sh_pose[g], A.cfg.min_corr, A.cfg.rot_eps,
+                                         A.cfg.trans_eps, &status);
+#endif
+#if RK_ICP_TIME_SOLVE
+        t_solve_acc += clock64() - t_solve0;
+#endif
+        if (gtid == 0) {
+          if (ctrl != 2) {
+            if (A.stats && n_done < A.stats_stride) {
+              double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
+              row[0] = stride;
+              row[1] = it;
+              row[2] = n_corr;
+              row[3] = kern * kern * tot[27];
+              row[4] = sqrt(tot[28] / n_corr);
+            }
+            ++n_done;
           }
-          ++n_done;
+          sh_ctrl[g] = ctrl;
         }
-        sh_ctrl[g] = ctrl;
       }
       group_sync<WPP>(g);
       const int ctrl = sh_ctrl[g];
@@ -372,6 +502,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     work += valid_lv * executed;
   }
 finish:
+#if RK_ICP_TIME_SOLVE
+  if (gtid == 0 && pair < 4)
+    printf("pair %d: solve %lld cycles of %lld total, %d iterations\n", pair, t_solve_acc,
+           clock64() - t_kernel0, n_done);
+#endif
   if (A.pt_iters) {
     const unsigned w = __reduce_add_sync(0xffffffffu, work);
     if (lane == 0 && w) atomicAdd(A.pt_iters, (unsigned long long)w);
