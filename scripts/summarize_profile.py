@@ -116,9 +116,10 @@ def main():
     lp = Path(a.launches or ROOT / "gpurun_out" / f"launches_{a.tag}.csv")
     if lp.exists():
         launches(a.tag, lp)
-    rp = Path(a.rep or ROOT / "gpurun_out" / f"prof_{a.tag}.ncu-rep")
-    if rp.exists():
-        full(a.tag, rp)
+    reps = [Path(a.rep)] if a.rep else sorted((ROOT / "gpurun_out").glob(f"prof_*{a.tag}.ncu-rep"))
+    for rp in reps:
+        name = rp.stem.replace("prof_", "").replace(f"_{a.tag}", "")
+        full(a.tag if name == a.tag else f"{a.tag}_{name}", rp)
 
 
 if __name__ == "__main__":
