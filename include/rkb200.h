@@ -203,6 +203,15 @@ int rk_grid_set_touched(rk_grid* g, const int32_t* keys, int64_t n, void* stream
 int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* range,
                       const double* inv12, float clip_min, float clip_max, int math,
                       int64_t* updated, void* stream);
+/* integrate_cloud_frame over F posed frames (sdf_volume.py:198-210 in a
+ * loop, cli.py:267-283): frames (F,H,W), poses12 / invs12 (F,12) frame->world
+ * and world->frame.  The activation of frame f+1 runs on an internal stream
+ * while frame f integrates (two touched-set slots); safe under stream capture.
+ * Afterwards the touched set is the last frame's. */
+int rk_grid_integrate_frames(rk_grid* g, const rk_sensor* s, const float* frames, int32_t n_frames,
+                             const double* poses12, const double* invs12, double radius,
+                             float clip_min, float clip_max, int math, int64_t* updated,
+                             void* stream);
 /* multi-GPU hash sharding: the grid only allocates blocks whose
  * owner(key) == rank; rk_block_owner is the host mirror of owner() for
  * keys_host (n,3).  Sharded integration needs the frame's global touched

@@ -78,6 +78,7 @@ SIGNATURES = {
     "rk_grid_activate_image": [_p, _p, _p, _p, _f64, _f32, _f32, _p],
     "rk_grid_set_touched": [_p, _p, _i64, _p],
     "rk_grid_integrate": [_p, _p, _p, _p, _f32, _f32, C.c_int, _p, _p],
+    "rk_grid_integrate_frames": [_p, _p, _p, _i32, _p, _p, _f64, _f32, _f32, C.c_int, _p, _p],
     "rk_grid_keys": [_p, C.c_int, _p, _i64, _p, _p],
     "rk_grid_read_blocks": [_p, _p, _i64, _p, _p, _p],
     "rk_grid_write_blocks": [_p, _p, _i64, _p, _p],

@@ -11,6 +11,14 @@
 
 using namespace rk;
 
+// K5 launch shape: RK_TSDF_THREADS x RK_TSDF_CTAS_PER_SM persistent CTAs per SM
+#ifndef RK_TSDF_THREADS
+#define RK_TSDF_THREADS 256
+#endif
+#ifndef RK_TSDF_CTAS_PER_SM
+#define RK_TSDF_CTAS_PER_SM 3  // leaves a quarter of the register file for the overlapped activation
+#endif
+
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
 namespace {
@@ -22,11 +30,16 @@ constexpr long long kShift = 1ll << 18;
 constexpr unsigned long long kEmpty = ~0ull;
 constexpr int kChunkBlocks = 600000 / kVox;  // sdf_volume.py:142 (146 blocks)
 
-struct Counters {
+// per-frame touched set bookkeeping; two slots so that the activation of
+// frame f+1 can run while frame f integrates (rk_grid_integrate_frames)
+struct TouchCounters {
   unsigned long long max_touched_key;  // largest packed key touched this frame
+  long long n_touched;
+};
+
+struct Counters {
   long long n_blocks;                  // allocated slots
   long long updated;                   // voxels updated by the last integrate
-  int n_touched;
   int n_fresh;
   int overflow;
   int n_points;                        // activation input size (gemv quirk)
@@ -60,9 +73,10 @@ struct GridDev {
   unsigned long long* h_keys;
   int32_t* h_slot;
   int32_t* h_stamp;
-  int32_t* touched;
+  int32_t* touched;      // this view's touched list (slot base + slot * hash capacity)
   int32_t* fresh;
   Counters* ctr;
+  TouchCounters* tc;     // this view's touched counters
   long long cap_blocks;
   unsigned long long hash_mask;
   int shard_rank, shard_world;  // multi-GPU: this grid keeps owner(key) == rank
@@ -116,8 +130,8 @@ __device__ __forceinline__ void touch_key(const GridDev& g, int frame, long long
   if (h < 0) { atomicExch(&g.ctr->overflow, 1); return; }
   if (inserted) g.fresh[atomicAdd(&g.ctr->n_fresh, 1)] = (int32_t)h;
   if (g.h_stamp[h] != frame && atomicExch(g.h_stamp + h, frame) != frame) {
-    g.touched[atomicAdd(&g.ctr->n_touched, 1)] = (int32_t)h;
-    atomicMax(&g.ctr->max_touched_key, key);
+    g.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&g.tc->n_touched), 1ull)] = (int32_t)h;
+    atomicMax(&g.tc->max_touched_key, key);
   }
 }
 
@@ -135,13 +149,13 @@ __device__ __forceinline__ void touch_point(const GridDev& g, int frame, const d
       for (long long z = lo[2]; z <= hi[2]; ++z) touch_key(g, frame, x, y, z);
 }
 
-__device__ __forceinline__ void reset_frame(Counters* c) {
+__device__ __forceinline__ void reset_frame(Counters* c, TouchCounters* t) {
   c->frame += 1;
-  c->n_touched = 0;
   c->n_fresh = 0;
-  c->max_touched_key = 0ull;
+  t->n_touched = 0;
+  t->max_touched_key = 0ull;
 }
-__global__ void k_reset_frame(Counters* c) { reset_frame(c); }
+__global__ void k_reset_frame(Counters* c, TouchCounters* t) { reset_frame(c, t); }
 
 // touch_point for a whole warp.  A warp is 32 neighbouring pixels of one
 // row, so its cubes share few block keys: lanes elect one lane per distinct
@@ -206,9 +220,10 @@ __global__ void k_activate_points(GridDev g, const double* __restrict__ pts, int
 // n_points, which the previous k_assign_slots left at zero
 constexpr int kBeginThreads = 256, kBeginCtas = 64;
 __global__ void __launch_bounds__(kBeginThreads) k_begin_image_frame(const float* __restrict__ range, int n,
-                                                                      float cmin, float cmax, Counters* c) {
+                                                                      float cmin, float cmax, Counters* c,
+                                                                      TouchCounters* t) {
   __shared__ int part[kBeginThreads / 32];
-  if (blockIdx.x == 0 && threadIdx.x == 0) reset_frame(c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) reset_frame(c, t);
   int cnt = 0;
   for (int i = blockIdx.x * kBeginThreads + threadIdx.x; i < n; i += kBeginThreads * gridDim.x)
     cnt += range_ok(__ldg(range + i), cmin, cmax) ? 1 : 0;
@@ -297,7 +312,7 @@ struct IntegrateArgs {
 // f32(((local + 0.5) * voxel) @ inv.R^T), the OpenBLAS FMA order) -- 36
 // float64 ops per thread instead of a separate launch and a 48 KB copy.
 template <int MATH, int NT, bool SMEM>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_integrate(IntegrateArgs A) {
+__global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(IntegrateArgs A) {
   extern __shared__ float sh_off[];  // kVox*3 rotated lattice (48 KB, dynamic)
   __shared__ int sh_cnt[NT / 32];
   __shared__ int sh_e;
@@ -321,14 +336,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_integrate(IntegrateArgs A) {
   }
   __syncthreads();
   const SensorDev& s = A.s;
-  const int n_touched = A.g.ctr->n_touched;
+  const int n_touched = (int)A.g.tc->n_touched;
   // the reference integrates sorted keys in chunks of 146 blocks; a chunk of a
   // single block goes through dgemv, which orders the FMA chain differently.
   // A hash-sharded grid needs the frame's global count / largest key, which
   // the caller all-reduces into global_touch = {count, max key}.
   const long long n_all = A.global_touch ? A.global_touch[0] : n_touched;
   const unsigned long long max_key =
-      A.global_touch ? (unsigned long long)A.global_touch[1] : A.g.ctr->max_touched_key;
+      A.global_touch ? (unsigned long long)A.global_touch[1] : A.g.tc->max_touched_key;
   const bool lone_tail = (n_all % kChunkBlocks) == 1;
   int count = 0;
   for (;;) {
@@ -410,8 +425,8 @@ __global__ void k_set_touched(GridDev g, const int32_t* __restrict__ keys, int64
   long long h = hash_find(g, key);
   if (h < 0) return;
   if (atomicExch(g.h_stamp + h, frame) != frame) {
-    g.touched[atomicAdd(&g.ctr->n_touched, 1)] = (int32_t)h;
-    atomicMax(&g.ctr->max_touched_key, key);
+    g.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&g.tc->n_touched), 1ull)] = (int32_t)h;
+    atomicMax(&g.tc->max_touched_key, key);
   }
 }
 
@@ -427,7 +442,7 @@ __global__ void k_keys_all(GridDev g, int32_t* out, long long cap) {
 }
 
 __global__ void k_keys_touched(GridDev g, int32_t* out, long long cap) {
-  int nt = g.ctr->n_touched;
+  const long long nt = g.tc->n_touched;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nt && i < cap;
        i += (long long)gridDim.x * blockDim.x) {
     int x, y, z;
@@ -535,11 +550,8 @@ __global__ void k_rehash(GridDev g, long long nb) {
 }  // namespace
 
 // ------------------------------------------------------------------ host side
-#ifndef RK_TSDF_THREADS
-#define RK_TSDF_THREADS 512
-#endif
 constexpr int kIntegrateThreads = RK_TSDF_THREADS;
-constexpr int kIntegrateCtasPerSm = 1024 / kIntegrateThreads;  // 64 registers x 1024 threads per SM
+constexpr int kIntegrateCtasPerSm = RK_TSDF_CTAS_PER_SM;
 constexpr size_t kLatticeBytes = kVox * 3 * sizeof(float);
 
 static int num_sms() {
@@ -568,20 +580,31 @@ struct rk_grid {
   double voxel, trunc;
   float max_weight;
   int free_space;
-  GridDev d;
+  GridDev d;              // slot-0 view; d.touched / d.tc are the bases of both slots
   unsigned long long hash_cap;
+  int last_slot = 0;      // touched-set slot of the most recent activation
   const long long* global_touch = nullptr;  // device {count, max key} (sharded grids)
+  cudaStream_t side = nullptr;               // activation stream of rk_grid_integrate_frames
+  cudaEvent_t ev_act[2] = {nullptr, nullptr}, ev_int[2] = {nullptr, nullptr}, ev_fork = nullptr;
 };
+
+// the grid as seen by the kernels of one touched-set slot
+static GridDev view(const rk_grid* g, int slot) {
+  GridDev v = g->d;
+  v.touched = g->d.touched + (size_t)slot * g->hash_cap;
+  v.tc = g->d.tc + slot;
+  return v;
+}
 
 // {n_touched, max touched key} of the last activation into a device int64[2]
 // (multi-GPU: all-reduce these with sum / max, then rk_grid_set_global_touch)
-__global__ void k_touch_stats(const Counters* c, long long* out) {
-  out[0] = c->n_touched;
-  out[1] = (long long)c->max_touched_key;
+__global__ void k_touch_stats(const TouchCounters* t, long long* out) {
+  out[0] = t->n_touched;
+  out[1] = (long long)t->max_touched_key;
 }
 
 extern "C" int rk_grid_touch_stats(rk_grid* g, int64_t* out2, void* stream) {
-  k_touch_stats<<<1, 1, 0, S(stream)>>>(g->d.ctr, reinterpret_cast<long long*>(out2));
+  k_touch_stats<<<1, 1, 0, S(stream)>>>(g->d.tc + g->last_slot, reinterpret_cast<long long*>(out2));
   RK_LAUNCHED("k_touch_stats");
   return RK_OK;
 }
@@ -609,7 +632,7 @@ static int alloc_tables(rk_grid* g, long long cap_blocks, cudaStream_t st) {
   RK_CUDA(cudaMemsetAsync(d.h_slot, 0xff, hcap * sizeof(int32_t), st));
   RK_CUDA(cudaMalloc(&d.h_stamp, hcap * sizeof(int32_t)));
   RK_CUDA(cudaMemsetAsync(d.h_stamp, 0, hcap * sizeof(int32_t), st));
-  RK_CUDA(cudaMalloc(&d.touched, hcap * sizeof(int32_t)));
+  RK_CUDA(cudaMalloc(&d.touched, 2 * hcap * sizeof(int32_t)));  // two touched-set slots
   RK_CUDA(cudaMalloc(&d.fresh, hcap * sizeof(int32_t)));
   d.cap_blocks = cap_blocks;
   d.hash_mask = hcap - 1;
@@ -643,9 +666,19 @@ extern "C" int rk_grid_create(double voxel_size, double truncation, float max_we
   if (capacity_blocks < 64) capacity_blocks = 64;
   int rc = alloc_tables(g, capacity_blocks, 0);
   if (rc) { delete g; return rc; }
-  RK_CUDA(cudaMalloc(&g->d.ctr, sizeof(Counters)));
-  RK_CUDA(cudaMemset(g->d.ctr, 0, sizeof(Counters)));
+  // counters and the two touched-set slots' counters in one allocation
+  RK_CUDA(cudaMalloc(&g->d.ctr, sizeof(Counters) + 2 * sizeof(TouchCounters)));
+  RK_CUDA(cudaMemset(g->d.ctr, 0, sizeof(Counters) + 2 * sizeof(TouchCounters)));
+  g->d.tc = reinterpret_cast<TouchCounters*>(g->d.ctr + 1);
   RK_CUDA(set_integrate_attrs());
+  // side stream + events of rk_grid_integrate_frames, created here so that the
+  // sequence call itself can run under stream capture
+  RK_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    RK_CUDA(cudaEventCreateWithFlags(&g->ev_act[i], cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&g->ev_int[i], cudaEventDisableTiming));
+  }
+  RK_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
   RK_CUDA(cudaDeviceSynchronize());
   *out = g;
   return RK_OK;
@@ -656,6 +689,11 @@ extern "C" int rk_grid_destroy(rk_grid* g) {
   cudaDeviceSynchronize();
   free_tables(g->d);
   cudaFree(g->d.ctr);
+  if (g->side) {
+    cudaStreamDestroy(g->side);
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(g->ev_act[i]); cudaEventDestroy(g->ev_int[i]); }
+    cudaEventDestroy(g->ev_fork);
+  }
   delete g;
   return RK_OK;
 }
@@ -679,9 +717,9 @@ extern "C" int rk_grid_reserve(rk_grid* g, int64_t capacity_blocks, void* stream
     RK_LAUNCHED("k_rehash");
   }
   c.overflow = 0;
-  c.n_touched = 0;
   c.n_fresh = 0;
   RK_CUDA(cudaMemcpyAsync(g->d.ctr, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+  RK_CUDA(cudaMemsetAsync(g->d.tc, 0, 2 * sizeof(TouchCounters), st));
   RK_CUDA(cudaStreamSynchronize(st));
   free_tables(old);
   return RK_OK;
@@ -690,16 +728,19 @@ extern "C" int rk_grid_reserve(rk_grid* g, int64_t capacity_blocks, void* stream
 extern "C" int rk_grid_info(rk_grid* g, int64_t* out4, void* stream) {
   cudaStream_t st = S(stream);
   Counters c;
+  TouchCounters t;
   RK_CUDA(cudaMemcpyAsync(&c, g->d.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+  RK_CUDA(cudaMemcpyAsync(&t, g->d.tc + g->last_slot, sizeof(t), cudaMemcpyDeviceToHost, st));
   RK_CUDA(cudaStreamSynchronize(st));
   out4[0] = c.n_blocks;
   out4[1] = g->d.cap_blocks;
   out4[2] = c.overflow;
-  out4[3] = c.n_touched;
+  out4[3] = t.n_touched;
   return RK_OK;
 }
 
 static int finish_activation(rk_grid* g, cudaStream_t st) {
+  g->last_slot = 0;
   k_assign_slots<<<1, kAssignThreads, 0, st>>>(g->d);
   RK_LAUNCHED("rk_grid activation");
   return RK_OK;
@@ -708,38 +749,47 @@ static int finish_activation(rk_grid* g, cudaStream_t st) {
 extern "C" int rk_grid_activate_points(rk_grid* g, const double* pts, int64_t n, double radius,
                                        void* stream) {
   cudaStream_t st = S(stream);
-  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr, g->d.tc);
   if (n > 0)
     k_activate_points<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, pts, n, radius,
                                                                     kEdge * g->voxel);
   return finish_activation(g, st);
 }
 
+// begin + activate + assign of one frame into touched-set slot `slot`
+static int activate_image_slot(rk_grid* g, const rk_sensor* s, const float* range, const double* pose12,
+                               double radius, float clip_min, float clip_max, int slot, cudaStream_t st) {
+  const int n = s->dev.H * s->dev.W;
+  const GridDev v = view(g, slot);
+  k_begin_image_frame<<<kBeginCtas, kBeginThreads, 0, st>>>(range, n, clip_min, clip_max, v.ctr, v.tc);
+  k_activate_image<<<(n + 255) / 256, 256, 0, st>>>(v, s->dev, range, pose12, radius,
+                                                    kEdge * g->voxel, clip_min, clip_max);
+  k_assign_slots<<<1, kAssignThreads, 0, st>>>(v);
+  RK_LAUNCHED("rk_grid activation");
+  return RK_OK;
+}
+
 extern "C" int rk_grid_activate_image(rk_grid* g, const rk_sensor* s, const float* range,
                                       const double* pose12, double radius, float clip_min,
                                       float clip_max, void* stream) {
-  cudaStream_t st = S(stream);
-  const int n = s->dev.H * s->dev.W;
-  k_begin_image_frame<<<kBeginCtas, kBeginThreads, 0, st>>>(range, n, clip_min, clip_max, g->d.ctr);
-  k_activate_image<<<(n + 255) / 256, 256, 0, st>>>(g->d, s->dev, range, pose12, radius,
-                                                    kEdge * g->voxel, clip_min, clip_max);
-  return finish_activation(g, st);
+  g->last_slot = 0;
+  return activate_image_slot(g, s, range, pose12, radius, clip_min, clip_max, 0, S(stream));
 }
 
 extern "C" int rk_grid_set_touched(rk_grid* g, const int32_t* keys, int64_t n, void* stream) {
   cudaStream_t st = S(stream);
-  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  g->last_slot = 0;
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr, g->d.tc);
   if (n > 0) k_set_touched<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, keys, n);
   RK_LAUNCHED("k_set_touched");
   return RK_OK;
 }
 
-extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* range,
-                                 const double* inv12, float clip_min, float clip_max, int math,
-                                 int64_t* updated, void* stream) {
-  cudaStream_t st = S(stream);
+static int integrate_slot(rk_grid* g, const rk_sensor* s, const float* range, const double* inv12,
+                          float clip_min, float clip_max, int math, int64_t* updated, int slot,
+                          cudaStream_t st) {
   IntegrateArgs a;
-  a.g = g->d;
+  a.g = view(g, slot);
   a.s = s->dev;
   a.range = range;
   a.inv12 = inv12;
@@ -766,16 +816,60 @@ extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* ra
   return RK_OK;
 }
 
+extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* range,
+                                 const double* inv12, float clip_min, float clip_max, int math,
+                                 int64_t* updated, void* stream) {
+  return integrate_slot(g, s, range, inv12, clip_min, clip_max, math, updated, g->last_slot,
+                        S(stream));
+}
+
+// F frames: activation of frame f+1 (side stream) overlaps the integration of
+// frame f (caller's stream).  Frame f uses touched-set slot f & 1; the
+// activation of f+2 waits for the integration of f (same slot), the
+// integration of f waits for its own activation.  Stream-capture safe (the
+// side stream forks from and joins the caller's stream through events).
+extern "C" int rk_grid_integrate_frames(rk_grid* g, const rk_sensor* s, const float* frames,
+                                        int32_t n_frames, const double* poses12, const double* invs12,
+                                        double radius, float clip_min, float clip_max, int math,
+                                        int64_t* updated, void* stream) {
+  cudaStream_t st = S(stream);
+  if (n_frames <= 0) return RK_OK;
+  const size_t px = (size_t)s->dev.H * s->dev.W;
+  RK_CUDA(cudaEventRecord(g->ev_fork, st));
+  RK_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
+  for (int f = 0; f < n_frames; ++f) {
+    const int slot = f & 1;
+    if (f >= 2) RK_CUDA(cudaStreamWaitEvent(g->side, g->ev_int[slot], 0));
+    int rc = activate_image_slot(g, s, frames + f * px, poses12 + 12 * f, radius, clip_min, clip_max,
+                                 slot, g->side);
+    if (rc) return rc;
+    RK_CUDA(cudaEventRecord(g->ev_act[slot], g->side));
+    RK_CUDA(cudaStreamWaitEvent(st, g->ev_act[slot], 0));
+    rc = integrate_slot(g, s, frames + f * px, invs12 + 12 * f, clip_min, clip_max, math, updated,
+                        slot, st);
+    if (rc) return rc;
+    RK_CUDA(cudaEventRecord(g->ev_int[slot], st));
+  }
+  // join: the caller's stream already waited for the last activation; make
+  // the side stream's tail (nothing after it) part of the caller's order too
+  RK_CUDA(cudaEventRecord(g->ev_act[0], g->side));
+  RK_CUDA(cudaStreamWaitEvent(st, g->ev_act[0], 0));
+  g->last_slot = (n_frames - 1) & 1;
+  return RK_OK;
+}
+
 extern "C" int rk_grid_keys(rk_grid* g, int touched_only, int32_t* keys_out, int64_t cap,
                             int64_t* n_host, void* stream) {
   cudaStream_t st = S(stream);
   Counters c;
+  TouchCounters t;
   RK_CUDA(cudaMemcpyAsync(&c, g->d.ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+  RK_CUDA(cudaMemcpyAsync(&t, g->d.tc + g->last_slot, sizeof(t), cudaMemcpyDeviceToHost, st));
   RK_CUDA(cudaStreamSynchronize(st));
-  long long n = touched_only ? c.n_touched : c.n_blocks;
+  long long n = touched_only ? t.n_touched : c.n_blocks;
   if (n_host) *n_host = n;
   if (keys_out && cap > 0 && n > 0) {
-    if (touched_only) k_keys_touched<<<128, 256, 0, st>>>(g->d, keys_out, cap);
+    if (touched_only) k_keys_touched<<<128, 256, 0, st>>>(view(g, g->last_slot), keys_out, cap);
     else k_keys_all<<<128, 256, 0, st>>>(g->d, keys_out, cap);
     RK_LAUNCHED("rk_grid_keys");
   }
@@ -794,7 +888,7 @@ extern "C" int rk_grid_write_blocks(rk_grid* g, const int32_t* keys, int64_t n, 
                                     void* stream) {
   cudaStream_t st = S(stream);
   if (n <= 0) return RK_OK;
-  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr);
+  k_reset_frame<<<1, 1, 0, st>>>(g->d.ctr, g->d.tc);
   k_insert_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->d, keys, n);
   int rc = finish_activation(g, st);
   if (rc) return rc;
@@ -835,14 +929,16 @@ __global__ void k_clear_blocks(GridDev g) {
        i += (long long)gridDim.x * blockDim.x)
     v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
-__global__ void k_clear_counters(Counters* c) {
+__global__ void k_clear_counters(Counters* c, TouchCounters* t) {
   c->n_blocks = 0;
-  c->n_touched = 0;
   c->n_fresh = 0;
   c->overflow = 0;
-  c->max_touched_key = 0ull;
   c->updated = 0;
   c->n_points = 0;
+  for (int i = 0; i < 2; ++i) {
+    t[i].n_touched = 0;
+    t[i].max_touched_key = 0ull;
+  }
 }
 }  // namespace
 
@@ -852,7 +948,7 @@ extern "C" int rk_grid_clear(rk_grid* g, void* stream) {
   k_clear_blocks<<<148 * 8, 256, 0, st>>>(g->d);
   RK_CUDA(cudaMemsetAsync(g->d.h_keys, 0xff, g->hash_cap * sizeof(unsigned long long), st));
   RK_CUDA(cudaMemsetAsync(g->d.h_slot, 0xff, g->hash_cap * sizeof(int32_t), st));
-  k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr);
+  k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr, g->d.tc);
   RK_LAUNCHED("rk_grid_clear");
   return RK_OK;
 }

@@ -69,9 +69,10 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
     Returns the device int64 counter of updated voxels.  The caller must size
     the grid (``grid.reserve``) and may check ``grid.info()`` for overflow.
 
-    graph=True records the 4*F launches once as a CUDA graph (keyed by the
-    buffers) and replays it on later calls with the same buffers: the frame
-    stamps live on the device, so a replay is an exact re-run.
+    The activation of frame f+1 (side stream) overlaps the integration of
+    frame f.  graph=True records the 4*F launches once as a CUDA graph (keyed
+    by the buffers) and replays it on later calls with the same buffers: the
+    frame stamps live on the device, so a replay is an exact re-run.
     """
     h = grid._prepare()
     sensor = lm.device_sensor(intr)
@@ -85,13 +86,15 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
     cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
     math = lm.default_math()
 
+    frames = frames.contiguous()
+    poses_w = poses_w.contiguous()
+    inv_w = inv_w.contiguous()
+
     def issue():
-        st = nat.stream_ptr()
-        for f in range(frames.shape[0]):
-            nat.call("rk_grid_activate_image", h, sensor, nat.ptr(frames[f]), nat.ptr(poses_w[f]),
-                     float(radius), cmin, cmax, st)
-            nat.call("rk_grid_integrate", h, sensor, nat.ptr(frames[f]), nat.ptr(inv_w[f]), cmin,
-                     cmax, math, nat.ptr(updated), st)
+        # activation of frame f+1 overlaps the integration of frame f
+        nat.call("rk_grid_integrate_frames", h, sensor, nat.ptr(frames), int(frames.shape[0]),
+                 nat.ptr(poses_w), nat.ptr(inv_w), float(radius), cmin, cmax, math,
+                 nat.ptr(updated), nat.stream_ptr())
 
     if not graph:
         issue()
