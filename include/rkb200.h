@@ -99,6 +99,19 @@ int rk_unproject_image(const rk_sensor* s, const float* range, int32_t batch,
  * be NULL.  surfel = {nx, ny, nz, range if valid else 0} (the ICP gather map). */
 int rk_normals_cross(const rk_sensor* s, const float* range, int32_t batch,
                      float* normals, uint8_t* valid, float* surfel, void* stream);
+/* compute_normal_map(method="pca")  range_image.py:243-283: smallest
+ * covariance eigenvector over the (2*radius+1)^2 window's valid neighbours
+ * within disc_abs + disc_rel * r; outputs as rk_normals_cross (any may be NULL). */
+int rk_normals_pca(const rk_sensor* s, const float* range, int32_t batch, int32_t radius,
+                   double disc_abs, double disc_rel, float* normals, uint8_t* valid, float* surfel,
+                   void* stream);
+/* from_point_cloud's z-buffer  range_image.py:170-194: given rk_project_f64's
+ * (u, v, r, status) of n points, the (H,W) float32 image of the nearest range
+ * per pixel (0 = empty) and stats4 = {kept, collisions, out_of_fov, degenerate}
+ * (device int64[4]).  zwork: H*W 64-bit scratch. */
+int rk_zbuffer_image(const rk_sensor* s, const double* u, const int32_t* v, const double* r,
+                     const int8_t* status, int64_t n, float* range_out, int64_t* stats4,
+                     unsigned long long* zwork, void* stream);
 /* StridedView + points_at_stride / to_point_cloud mask, range_image.py:69-157:
  * row-major flat base-pixel indices (v*W+u) of the stride-s view whose range
  * passes r>0 & clip_min<=r<=clip_max, per image; idx has capacity

@@ -1,4 +1,5 @@
-"""Oracle: range-image operations (point clouds, pyramid views, cross normals).
+"""Oracle: range-image operations (point clouds, pyramid views, cross and PCA
+normals, cloud -> image z-buffer).
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Restates
 ``rangekit/range_image.py``; citations are to that file.
@@ -93,3 +94,49 @@ def from_point_cloud(sensor, points, max_iters=3, tol=1e-4):
         stats["collisions"] = n_in - n_pix
     buf[~np.isfinite(buf)] = 0.0
     return buf.reshape(H, W).astype(F32), stats
+
+
+def normals_pca(sensor, rng, radius=2, disc_abs=0.3, disc_rel=0.05):
+    """Windowed-PCA normals (243-283): float64 window sums in the (dv, du)
+    order, covariance, numpy eigh's smallest eigenvector, sensor-facing.
+
+    Returns (vectors float32 (H,W,3), valid bool (H,W)).
+    """
+    r32 = np.asarray(rng, dtype=F32)
+    P = sensor.unproject_image(r32)
+    valid = r32 > 0
+    r = r32.astype(np.float64)
+    H, W = r.shape
+    count = np.zeros((H, W))
+    s1 = np.zeros((H, W, 3))
+    s2 = np.zeros((H, W, 3, 3))
+    thresh = disc_abs + disc_rel * r
+    for dv in range(-radius, radius + 1):
+        for du in range(-radius, radius + 1):
+            q = np.roll(P, -du, axis=1)
+            qv = np.roll(valid, -du, axis=1)
+            qr = np.roll(r, -du, axis=1)
+            if dv:
+                q2 = np.zeros_like(q)
+                qv2 = np.zeros_like(qv)
+                qr2 = np.zeros_like(qr)
+                if dv > 0:
+                    q2[:-dv], qv2[:-dv], qr2[:-dv] = q[dv:], qv[dv:], qr[dv:]
+                else:
+                    q2[-dv:], qv2[-dv:], qr2[-dv:] = q[:dv], qv[:dv], qr[:dv]
+                q, qv, qr = q2, qv2, qr2
+            w = (valid & qv & (np.abs(qr - r) <= thresh)).astype(np.float64)
+            count += w
+            s1 += w[..., None] * q
+            s2 += w[..., None, None] * (q[..., :, None] * q[..., None, :])
+    ok = valid & (count >= 3)
+    n = np.zeros((H, W, 3))
+    if np.any(ok):
+        c = count[ok][:, None]
+        mean = s1[ok] / c
+        cov = s2[ok] / c[..., None] - mean[:, :, None] * mean[:, None, :]
+        n[ok] = np.linalg.eigh(cov)[1][:, :, 0]
+    flip = np.sum(n * P, axis=-1) > 0
+    n[flip] = -n[flip]
+    n[~ok] = 0.0
+    return n.astype(F32), ok

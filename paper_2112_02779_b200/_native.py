@@ -54,6 +54,8 @@ SIGNATURES = {
     "rk_unproject_image": [_p, _p, _i32, _p, _p],
     "rk_normals_cross": [_p, _p, _i32, _p, _p, _p, _p],
     "rk_stride_compact": [_p, _p, _i32, _i32, _f32, _f32, _p, _p, _p],
+    "rk_normals_pca": [_p, _p, _i32, _i32, _f64, _f64, _p, _p, _p, _p],
+    "rk_zbuffer_image": [_p, _p, _p, _p, _p, _i64, _p, _p, _p, _p],
     "rk_unproject_pixels": [_p, _p, _p, _p, _i64, _p, _p],
     "rk_compact_mask": [_p, _i64, _p, _p, _p],
     "rk_correspondences_f32": [_p, _p, _i64, _p, _p, _p, _f64, _i32, C.c_int, _p, _p, _p, _p],

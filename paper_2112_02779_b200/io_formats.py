@@ -15,7 +15,7 @@ import numpy as np
 from .errors import FormatError, InvalidIntrinsics, TruncatedPayload
 from .lidar_model import MODE_CALIBRATED, MODE_SYNTHETIC, LidarIntrinsics, synthetic_intrinsics
 from .range_image import RangeImage
-from .sdf_volume import BLOCK_EDGE, VoxelBlock, VoxelBlockGrid
+from .sdf_volume import BLOCK_EDGE, VoxelBlockGrid
 
 RIMG_MAGIC = b"RIMG"
 GRID_MAGIC = b"SDFG"
@@ -91,22 +91,25 @@ def read_range_image(path, intr: LidarIntrinsics | None = None) -> RangeImage:
     return RangeImage(parse_range_image(blob, intr), intr)
 
 
+_BLOCK_REC = np.dtype([("key", "<i4", (3,)), ("vox", "<f4", (BLOCK_EDGE ** 3, 2))])
+
+
 def write_grid(path, grid: VoxelBlockGrid) -> None:
-    """SDFG snapshot, blocks sorted by key (io_formats.py:267-277)."""
-    items = sorted(grid.blocks.items())
+    """SDFG snapshot, blocks sorted by key (io_formats.py:267-277; formats.md
+    "SDFG"): one bulk device read-back, one write."""
+    keys, vox = grid.export_blocks()
+    rec = np.empty(keys.shape[0], dtype=_BLOCK_REC)
+    rec["key"] = keys
+    rec["vox"] = vox
     with open(path, "wb") as f:
         f.write(GRID_MAGIC)
-        f.write(struct.pack("<ddQ", grid.voxel_size, grid.truncation, len(items)))
-        for key, blk in items:
-            f.write(struct.pack("<iii", *key))
-            pair = np.empty((BLOCK_EDGE ** 3, 2), dtype="<f4")
-            pair[:, 0] = blk.tsdf.reshape(-1)
-            pair[:, 1] = blk.weight.reshape(-1)
-            f.write(pair.tobytes())
+        f.write(struct.pack("<ddQ", grid.voxel_size, grid.truncation, keys.shape[0]))
+        f.write(rec.tobytes())
 
 
 def read_grid(path) -> VoxelBlockGrid:
-    """io_formats.py:280-308."""
+    """io_formats.py:280-308: validation with byte offsets, then one bulk
+    device upload."""
     with open(path, "rb") as f:
         blob = f.read()
     if blob[:4] != GRID_MAGIC:
@@ -116,45 +119,43 @@ def read_grid(path) -> VoxelBlockGrid:
     voxel, trunc, n = struct.unpack_from("<ddQ", blob, 4)
     if not (np.isfinite(voxel) and voxel > 0 and np.isfinite(trunc) and trunc > 0):
         raise FormatError("invalid voxel size or truncation", offset=4)
-    per = 12 + 8 * BLOCK_EDGE ** 3
+    per = _BLOCK_REC.itemsize
     if len(blob) < 28 + n * per:
         raise TruncatedPayload(f"grid declares {n} blocks", offset=len(blob))
+    rec = np.frombuffer(blob, dtype=_BLOCK_REC, count=n, offset=28)
+    bad = ~np.isfinite(rec["vox"][..., 0]).all(axis=1) | (rec["vox"][..., 1] < 0).any(axis=1)
+    if np.any(bad):
+        first = int(np.flatnonzero(bad)[0])
+        raise FormatError("non-finite tsdf or negative weight in block", offset=28 + first * per + 12)
     grid = VoxelBlockGrid(voxel_size=voxel, truncation=trunc, capacity=max(1024, 2 * int(n)))
-    pos = 28
-    for _ in range(n):
-        key = struct.unpack_from("<iii", blob, pos)
-        pair = np.frombuffer(blob, dtype="<f4", count=2 * BLOCK_EDGE ** 3, offset=pos + 12).reshape(-1, 2)
-        tsdf = pair[:, 0].reshape((BLOCK_EDGE,) * 3).copy()
-        weight = pair[:, 1].reshape((BLOCK_EDGE,) * 3).copy()
-        if np.any(~np.isfinite(tsdf)) or np.any(weight < 0):
-            raise FormatError("non-finite tsdf or negative weight in block", offset=pos + 12)
-        grid.blocks[tuple(int(k) for k in key)] = VoxelBlock(tsdf, weight)
-        pos += per
+    grid.import_blocks(rec["key"], rec["vox"])
     return grid
 
 
 def write_ply(path, mesh_or_points, normals=None) -> None:
-    """Binary little-endian PLY (io_formats.py:169-199)."""
+    """Binary little-endian PLY (io_formats.py:169-199): float32 vertex records
+    (+ normals), then uchar-count + 3 x int32 face records."""
     from .mesh_extract import TriangleMesh
 
-    if isinstance(mesh_or_points, TriangleMesh):
-        verts, tris = mesh_or_points.vertices, mesh_or_points.triangles
-        normals = mesh_or_points.normals if normals is None else normals
-    else:
-        verts, tris = np.asarray(mesh_or_points, dtype=float).reshape(-1, 3), None
-    header = ["ply", "format binary_little_endian 1.0", f"element vertex {verts.shape[0]}",
-              "property float x", "property float y", "property float z"]
-    if normals is not None:
-        header += ["property float nx", "property float ny", "property float nz"]
+    mesh = isinstance(mesh_or_points, TriangleMesh)
+    verts = mesh_or_points.vertices if mesh else np.asarray(mesh_or_points, dtype=float).reshape(-1, 3)
+    tris = mesh_or_points.triangles if mesh else None
+    if mesh and normals is None:
+        normals = mesh_or_points.normals
+    fields = ["x", "y", "z"] + (["nx", "ny", "nz"] if normals is not None else [])
+    vrec = np.empty(verts.shape[0], dtype=[(f, "<f4") for f in fields])
+    cols = np.hstack([verts, normals]) if normals is not None else verts
+    for i, f in enumerate(fields):
+        vrec[f] = cols[:, i]
+    lines = ["ply", "format binary_little_endian 1.0", f"element vertex {verts.shape[0]}"]
+    lines += [f"property float {f}" for f in fields]
     if tris is not None:
-        header += [f"element face {tris.shape[0]}", "property list uchar int vertex_indices"]
-    header.append("end_header")
+        lines += [f"element face {tris.shape[0]}", "property list uchar int vertex_indices"]
+    lines.append("end_header")
+    payload = [("\n".join(lines) + "\n").encode("ascii"), vrec.tobytes()]
+    if tris is not None and tris.shape[0]:
+        frec = np.empty(tris.shape[0], dtype=[("n", "u1"), ("idx", "<i4", (3,))])
+        frec["n"], frec["idx"] = 3, tris
+        payload.append(frec.tobytes())
     with open(path, "wb") as f:
-        f.write(("\n".join(header) + "\n").encode("ascii"))
-        body = np.hstack([verts, normals]) if normals is not None else verts
-        f.write(body.astype("<f4").tobytes())
-        if tris is not None and tris.shape[0]:
-            rec = np.zeros(tris.shape[0], dtype=[("n", "u1"), ("idx", "<i4", (3,))])
-            rec["n"] = 3
-            rec["idx"] = tris
-            f.write(rec.tobytes())
+        f.write(b"".join(payload))

@@ -274,8 +274,27 @@ def compute_normal_map(img: RangeImage, method: str = "cross", radius: int = 2,
     if method == "cross":
         return normals_cross(img)
     if method == "pca":
-        raise NotImplementedError("pca normals are SURVEY §8(f) N3 (next round)")
+        return normals_pca(img, radius, discontinuity_abs, discontinuity_rel)
     raise ValueError(f"unknown normal method {method!r}")
+
+
+def normals_pca(img: RangeImage, radius: int = 2, discontinuity_abs: float = DISCONTINUITY_ABS,
+                discontinuity_rel: float = DISCONTINUITY_REL) -> NormalImage:
+    """Windowed-PCA normals (range_image.py:243-283): smallest covariance
+    eigenvector over the valid neighbours of a (2*radius+1)^2 window that are
+    not across a depth discontinuity; invalid with fewer than 3 of them."""
+    intr = _require_intrinsics(img)
+    rng = img.device_data()
+    H, W = intr.height, intr.width
+    vec = nat.empty((H, W, 3), np.float32)
+    val = nat.empty((H, W), np.uint8)
+    surf = nat.empty((H, W, 4), np.float32)
+    nat.call("rk_normals_pca", lm.device_sensor(intr), nat.ptr(rng), 1, int(radius),
+             float(discontinuity_abs), float(discontinuity_rel), nat.ptr(vec), nat.ptr(val),
+             nat.ptr(surf), nat.stream_ptr())
+    if img.on_device:
+        return NormalImage(vec, val.bool(), surf)
+    return NormalImage(nat.to_host(vec), nat.to_host(val).astype(bool), surf)
 
 
 def normals_cross(img: RangeImage) -> NormalImage:
@@ -302,5 +321,40 @@ def normals_cross_batch(intr: LidarIntrinsics, ranges):
     return surf
 
 
+@dataclass
+class ProjectionStats:
+    """Bookkeeping from from_point_cloud (range_image.py:119-126)."""
+
+    kept: int = 0
+    collisions: int = 0
+    out_of_fov: int = 0
+    degenerate: int = 0
+
+
 def from_point_cloud(points, intr: LidarIntrinsics, max_iters: int = 3, tol: float = 1e-4):
-    raise NotImplementedError("from_point_cloud is SURVEY §8(f) N1 (next round)")
+    """Project a cloud into a fresh image, nearest range wins pixel collisions
+    (range_image.py:170-194): the float64 projection (rk_project_f64) then a
+    64-bit atomicMin z-buffer (rk_zbuffer_image).  Returns (RangeImage,
+    ProjectionStats); the image stays on the device for device input."""
+    on_dev = _is_dev(points)
+    pts = nat.to_dev(points, np.float64).reshape(-1, 3)
+    n = int(pts.shape[0])
+    H, W = intr.height, intr.width
+    sensor = lm.device_sensor(intr)
+    st = nat.stream_ptr()
+    u = nat.empty((max(n, 1),), np.float64)
+    v = nat.empty((max(n, 1),), np.int32)
+    r = nat.empty((max(n, 1),), np.float64)
+    status = nat.empty((max(n, 1),), np.int8)
+    if n:
+        work = nat.empty((3 * n + 4,), np.float64)
+        nat.call("rk_project_f64", sensor, nat.ptr(pts), n, int(max_iters), float(tol), 1,
+                 nat.ptr(u), nat.ptr(v), nat.ptr(r), nat.ptr(status), nat.ptr(work), st)
+    out = nat.empty((H, W), np.float32)
+    stats = nat.zeros((4,), np.int64)
+    zb = nat.empty((H * W,), np.int64)
+    nat.call("rk_zbuffer_image", sensor, nat.ptr(u), nat.ptr(v), nat.ptr(r), nat.ptr(status), n,
+             nat.ptr(out), nat.ptr(stats), nat.ptr(zb), st)
+    k = [int(x) for x in nat.to_host(stats)]
+    ps = ProjectionStats(kept=k[0], collisions=k[1], out_of_fov=k[2], degenerate=k[3])
+    return RangeImage(out if on_dev else nat.to_host(out), intr), ps

@@ -64,6 +64,11 @@ def golden_mesh():
 
 
 @pytest.fixture(scope="session")
+def golden_next():
+    return Golden("next")
+
+
+@pytest.fixture(scope="session")
 def sensors():
     from paper_2112_02779_b200 import scenes
     return {"small": scenes.small_calib(), "synth": scenes.synth_intr(), "ouster": scenes.ouster64()}

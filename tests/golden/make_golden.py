@@ -231,12 +231,63 @@ def gen_mesh():
     np.savez_compressed(OUT / "mesh.npz", **out)
 
 
+def gen_next(pairs):
+    """N1 from_point_cloud, N2 SDFG / PLY bytes, N3 PCA normals."""
+    import tempfile
+
+    from rangekit import io_formats
+    from rangekit.range_image import from_point_cloud
+    out = {}
+    g = np.random.default_rng(77)
+    for name in ("room", "street"):
+        intr, ri, src, dst, gt = pairs[name]
+        cloud = to_point_cloud(rk.RangeImage(dst, ri))
+        pick = g.choice(cloud.shape[0], size=min(12000, cloud.shape[0]), replace=False)
+        pts = cloud[pick] + g.normal(scale=0.004, size=(len(pick), 3))
+        dup = pts[:1500] + g.normal(scale=0.002, size=(1500, 3))      # pixel collisions
+        extra = np.array([[0.0, 0.0, 0.0], [1e-3, 0.0, 0.0], [0.0, 0.0, 5.0], [0.1, 0.0, -8.0],
+                          [3.0, 2.0, 40.0]])                             # degenerate / out of FoV
+        pts = np.concatenate([pts, dup, extra])
+        img, st = from_point_cloud(pts, ri)
+        out[f"{name}/fpc_in"], out[f"{name}/fpc_img"] = pts, img.data
+        out[f"{name}/fpc_stats"] = np.array([st.kept, st.collisions, st.out_of_fov, st.degenerate])
+    for name in ("room", "synth"):
+        intr, ri, src, dst, gt = pairs[name]
+        nm = compute_normal_map(rk.RangeImage(dst, ri), "pca")
+        out[f"{name}/pca_nrm"], out[f"{name}/pca_valid"] = nm.vectors, nm.valid
+        nm3 = compute_normal_map(rk.RangeImage(dst, ri), "pca", radius=1, discontinuity_abs=0.1,
+                                 discontinuity_rel=0.02)
+        out[f"{name}/pca1_nrm"], out[f"{name}/pca1_valid"] = nm3.vectors, nm3.valid
+        res = registration.register(rk.RangeImage(src, ri), rk.RangeImage(dst, ri),
+                                    config=registration.RegistrationConfig(normal_method="pca"))
+        out[f"{name}/pca_reg_pose"] = res.pose.matrix()
+        out[f"{name}/pca_reg_stats"] = np.array([[s.stride, s.iteration, s.n_correspondences]
+                                                 for s in res.stats])
+    # N2: on-disk formats, byte for byte
+    small, rs = sensors()["small"], ref_intr(sensors()["small"])
+    room = ref_scene(scenes.room_scene())
+    poses = [scenes.perturbation_pose(np.random.default_rng(40 + i), 3.0, 0.3) for i in range(3)]
+    grid = sdf_volume.VoxelBlockGrid(voxel_size=0.2)
+    for p in poses:
+        sdf_volume.integrate_cloud_frame(grid, rk.RangeImage(render_scene(room, rs, ref_pose(p)).data, rs),
+                                         ref_pose(p), clip_max=12.0)
+    with tempfile.TemporaryDirectory() as d:
+        io_formats.write_grid(Path(d) / "g.sdfg", grid)
+        out["sdfg_bytes"] = np.frombuffer((Path(d) / "g.sdfg").read_bytes(), np.uint8)
+        m = np.load(OUT / "mesh.npz")
+        mesh = mesh_extract.TriangleMesh(m["sphere_V"], m["sphere_T"], m["sphere_N"])
+        io_formats.write_ply(Path(d) / "m.ply", mesh)
+        out["ply_bytes"] = np.frombuffer((Path(d) / "m.ply").read_bytes(), np.uint8)
+    np.savez_compressed(OUT / "next.npz", **out)
+
+
 def main():
     gen_sensor_and_projection()
     pairs = render_pairs()
     gen_images_icp(pairs)
     gen_tsdf(pairs)
     gen_mesh()
+    gen_next(pairs)
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
 

@@ -518,3 +518,88 @@ def test_mesh_empty_and_uniform(rk):
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) rows
+
+@pytest.mark.parametrize("pair", ("room", "street"))
+def test_from_point_cloud_vs_reference(rk, pair, sensors, golden_next):
+    """N1: float64 projection + atomicMin z-buffer against the reference's
+    from_point_cloud (device float64 atan2/sin/cos may differ from numpy's in
+    the last ulp, so a pixel may rarely change hands)."""
+    g = golden_next
+    img, st = rk.from_point_cloud(g[f"{pair}/fpc_in"], sensors[SENSOR_OF[pair]])
+    ref = g[f"{pair}/fpc_img"]
+    assert img.data.dtype == np.float32 and img.data.shape == ref.shape
+    assert np.mean(img.data == ref) >= 0.9999
+    assert np.abs(img.data - ref).max() <= 1e-4 or np.mean(img.data != ref) < 1e-4
+    k = g[f"{pair}/fpc_stats"]
+    assert (st.out_of_fov, st.degenerate) == (int(k[2]), int(k[3]))
+    assert abs(st.kept - int(k[0])) <= 2 and abs(st.collisions - int(k[1])) <= 2
+    assert st.kept + st.collisions == int(k[0] + k[1])
+
+
+def test_from_point_cloud_device_and_empty(rk, sensors):
+    import torch
+    intr = sensors["small"]
+    img, st = rk.from_point_cloud(np.zeros((0, 3)), intr)
+    assert not img.data.any() and (st.kept, st.collisions, st.out_of_fov, st.degenerate) == (0, 0, 0, 0)
+    pts = torch.tensor([[5.0, 0.0, 0.0], [5.0, 0.001, 0.0], [6.0, 0.0, 0.0]], device="cuda",
+                       dtype=torch.float64)
+    img, st = rk.from_point_cloud(pts, intr)
+    assert img.on_device
+    assert st.kept + st.collisions == 3 and st.kept >= 1
+    assert float(img.data[img.data > 0].min()) < 5.1      # nearest range wins
+
+
+@pytest.mark.parametrize("pair", ("room", "synth"))
+def test_pca_normals_vs_reference(rk, pair, sensors, golden_icp, golden_next):
+    """N3: valid masks exactly (window counts are exact arithmetic), normals
+    within 1e-5 of numpy's eigh wherever the smallest eigenvalue is separated."""
+    g = golden_next
+    img = rk.RangeImage(golden_icp[f"{pair}/dst"], sensors[SENSOR_OF[pair]])
+    for key, kw in (("pca", {}), ("pca1", dict(radius=1, discontinuity_abs=0.1,
+                                                discontinuity_rel=0.02))):
+        nm = rk.compute_normal_map(img, "pca", **kw)
+        assert np.array_equal(nm.valid, g[f"{pair}/{key}_valid"])
+        d = np.abs(nm.vectors - g[f"{pair}/{key}_nrm"]).max(axis=-1)[nm.valid]
+        assert np.mean(d <= 1e-5) >= 0.999, (key, np.mean(d <= 1e-5))
+
+
+@pytest.mark.parametrize("pair", ("room", "synth"))
+def test_register_pca_normals_vs_reference(rk, pair, sensors, golden_icp, golden_next):
+    g = golden_next
+    intr = sensors[SENSOR_OF[pair]]
+    res = rk.register(rk.RangeImage(golden_icp[f"{pair}/src"], intr),
+                      rk.RangeImage(golden_icp[f"{pair}/dst"], intr),
+                      config=rk.RegistrationConfig(normal_method="pca"))
+    M = g[f"{pair}/pca_reg_pose"]
+    assert rot_err(res.pose.R, M[:3, :3]) < 1e-5 and np.linalg.norm(res.pose.t - M[:3, 3]) < 1e-5
+    got = np.array([[s.stride, s.iteration] for s in res.stats])
+    assert np.array_equal(got, g[f"{pair}/pca_reg_stats"][:, :2])
+
+
+def test_sdfg_round_trip_bytes_and_values(rk, sensors, golden_tsdf, golden_next, tmp_path):
+    """N2: the reference's SDFG snapshot loads into the device grid and writes
+    back byte for byte; a grid integrated on the device exports the same key
+    set with values within the TSDF tolerance."""
+    from paper_2112_02779_b200 import io_formats
+    blob = golden_next["sdfg_bytes"].tobytes()
+    (tmp_path / "ref.sdfg").write_bytes(blob)
+    grid = io_formats.read_grid(tmp_path / "ref.sdfg")
+    io_formats.write_grid(tmp_path / "back.sdfg", grid)
+    assert (tmp_path / "back.sdfg").read_bytes() == blob
+    mine, _ = _seq_grid(rk, sensors, golden_tsdf)
+    io_formats.write_grid(tmp_path / "mine.sdfg", mine)
+    a = io_formats.read_grid(tmp_path / "mine.sdfg").export_blocks()
+    b = grid.export_blocks()
+    assert np.array_equal(a[0], b[0])
+    same_w = a[1][..., 1] == b[1][..., 1]
+    assert np.mean(same_w) >= 0.9999
+    assert np.mean(np.abs(a[1][..., 0] - b[1][..., 0])[same_w] <= 1e-5) >= 0.9999
+    with pytest.raises(rk.FormatError):
+        (tmp_path / "bad.sdfg").write_bytes(b"XXXX" + blob[4:])
+        io_formats.read_grid(tmp_path / "bad.sdfg")
+    with pytest.raises(rk.TruncatedPayload):
+        (tmp_path / "short.sdfg").write_bytes(blob[:100])
+        io_formats.read_grid(tmp_path / "short.sdfg")
