@@ -186,7 +186,7 @@ def run_ours(args, rank, world, dist):
     def step(timed):
         e = ev["normals"]
         e[0].record(stream)
-        surf = normals_cross_batch(intr, D["dst"])
+        surf = normals_cross_batch(intr, D["dst"], strides=[s for s, _ in cfg.schedule])
         e[1].record(stream)
         ev["icp"][0].record(stream)
         res = rk.register_batch(intr, D["src"], D["dst"], surf, pair_src=D["pair_idx"],
@@ -280,7 +280,7 @@ def run_e2e(args, rank, world, dist, D, tsdf, cfg):
         src.copy_(src_h, non_blocking=True)
         dst.copy_(dst_h, non_blocking=True)
         frames.copy_(frames_h, non_blocking=True)
-        surf = normals_cross_batch(intr, dst)
+        surf = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
         res = rk.register_batch(intr, src, dst, surf, pair_src=D["pair_idx"], pair_dst=D["pair_idx"],
                                 config=cfg)
         upd.zero_()

@@ -112,6 +112,14 @@ int rk_normals_pca(const rk_sensor* s, const float* range, int32_t batch, int32_
 int rk_zbuffer_image(const rk_sensor* s, const double* u, const int32_t* v, const double* r,
                      const int8_t* status, int64_t n, float* range_out, int64_t* stats4,
                      unsigned long long* zwork, void* stream);
+/* rk_normals_cross's surfel map as a pyramid: per image, the full map (H*W
+ * float4) followed by the decimated map of every stride in strides_host that
+ * is > 1 (ceil(H/s) x ceil(W/s), pixel (i, j) = full (i*s, j*s)), in order;
+ * pitch = H*W + sum of the decimated sizes.  The registration's coarse levels
+ * then gather from compact maps instead of every s-th pixel. */
+int rk_normals_cross_pyramid(const rk_sensor* s, const float* range, int32_t batch,
+                             const int32_t* strides_host, int32_t n_strides, float* surfel_pyr,
+                             int64_t pitch, void* stream);
 /* StridedView + points_at_stride / to_point_cloud mask, range_image.py:69-157:
  * row-major flat base-pixel indices (v*W+u) of the stride-s view whose range
  * passes r>0 & clip_min<=r<=clip_max, per image; idx has capacity
@@ -138,6 +146,12 @@ typedef struct {
   int32_t min_corr;
   int32_t scale_with_stride;
   int32_t math;            /* RK_MATH_* */
+  /* destination surfel layout: 0 = one (H*W) map per image, gathered at
+   * stride-aligned pixels; else the per-image pitch (pixels) of a surfel
+   * pyramid (rk_normals_cross_pyramid) and, per level, the pixel offset of
+   * its decimated map (< 0: use the full-resolution map at offset 0). */
+  int64_t surfel_pitch;
+  int32_t surfel_level_off[8];
 } rk_icp_config;
 
 /* projective_correspondences(single=True)  registration.py:117-187 for one

@@ -37,7 +37,8 @@ class IcpConfig(C.Structure):
     _fields_ = [("kernel_scale", _f64), ("max_dist", _f64), ("rot_eps", _f64),
                 ("trans_eps", _f64), ("clip_min", _f32), ("clip_max", _f32),
                 ("n_levels", _i32), ("strides", _i32 * 8), ("iters", _i32 * 8),
-                ("min_corr", _i32), ("scale_with_stride", _i32), ("math", _i32)]
+                ("min_corr", _i32), ("scale_with_stride", _i32), ("math", _i32),
+                ("surfel_pitch", _i64), ("surfel_level_off", _i32 * 8)]
 
 
 # name -> argtypes (restype is always int status)
@@ -54,6 +55,7 @@ SIGNATURES = {
     "rk_unproject_image": [_p, _p, _i32, _p, _p],
     "rk_normals_cross": [_p, _p, _i32, _p, _p, _p, _p],
     "rk_stride_compact": [_p, _p, _i32, _i32, _f32, _f32, _p, _p, _p],
+    "rk_normals_cross_pyramid": [_p, _p, _i32, _p, _i32, _p, _i64, _p],
     "rk_normals_pca": [_p, _p, _i32, _i32, _f64, _f64, _p, _p, _p, _p],
     "rk_zbuffer_image": [_p, _p, _p, _p, _p, _i64, _p, _p, _p, _p],
     "rk_unproject_pixels": [_p, _p, _p, _p, _i64, _p, _p],

@@ -254,8 +254,9 @@ template <int MATH, bool SMEM, bool STATS>
 __device__ __forceinline__ void associate_point(const SensorDev& s, const RowTables& tb,
                                                 const double* pose, float r, const double3& dcur,
                                                 const double3& ocur, const float4* surf, int stride,
-                                                float inv_s, float gate2, float inv_k, float* acc,
-                                                float& cost, float& sumsq, int& cnt) {
+                                                int lvl_off, int lvl_w, float inv_s, float gate2,
+                                                float inv_k, float* acc, float& cost, float& sumsq,
+                                                int& cnt) {
   const double rd = (double)r;
   double m[3];
   xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
@@ -263,12 +264,14 @@ __device__ __forceinline__ void associate_point(const SensorDev& s, const RowTab
   const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
   const Proj32 pr = project_f32<MATH, SMEM>(s, tb, mx, my, mz);
   if (pr.status != PROJ_OK) return;
-  int col = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f) * stride;
-  if (col >= s.W) col = 0;
-  const int row = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f) * stride;
+  int ci = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f);
+  if (ci * stride >= s.W) ci = 0;
+  const int ri = (int)__fadd_rn(__fmul_rn((float)pr.v, inv_s), 0.5f);
+  const int col = ci * stride, row = ri * stride;
   if (row >= s.H) return;  // dropped, not clamped (registration.py:157-159)
   const int flat = row * s.W + col;
-  const float4 n = __ldg(surf + flat);
+  // the level's compact decimated map when the caller built a pyramid
+  const float4 n = __ldg(surf + (lvl_w ? lvl_off + ri * lvl_w + ci : flat));
   const float4 d = __ldg(s.dirs32 + flat);
   const float4 o = __ldg(s.origins32 + col);
   accumulate_point<STATS>(mx, my, mz, n, d, o, gate2, inv_k, acc, cost, sumsq, cnt);
@@ -305,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   const int H = s.H, W = s.W;
   const size_t HW = (size_t)H * W;
   const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
-  const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * HW;
+  const long long surf_pitch = A.cfg.surfel_pitch ? A.cfg.surfel_pitch : (long long)HW;
+  const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * surf_pitch;
 
   __shared__ double sh_pose[GROUPS][12];
   __shared__ double sh_red[NW][kNumAcc];
@@ -340,6 +344,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     const int vi0 = gtid / Ws, ui0 = gtid - vi0 * Ws;
     const int off0 = vi0 * stride * W + ui0 * stride;
     const bool col_mode = Ws % GT == 0;
+    const int lvl_off = A.cfg.surfel_pitch ? A.cfg.surfel_level_off[lv] : 0;
+    const int lvl_w = (A.cfg.surfel_pitch && lvl_off > 0) ? Ws : 0;
     const int row_step = stride * W;
     // executed work (the roofline's unit) = valid points of this level x the
     // iterations run; counted once per level, outside the hot loop
@@ -387,8 +393,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
               d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
             }
             if (!range_ok(r, cmin, cmax)) continue;
-            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, inv_s, gate2,
-                                               inv_k, acc, cost, sumsq, cnt);
+            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, lvl_off,
+                                               lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
           }
         }
       } else {
@@ -416,8 +422,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           if (!range_ok(r, cmin, cmax)) continue;
           const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
                                             __ldg(s.origins + 3 * u + 2));
-          associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, inv_s, gate2,
-                                             inv_k, acc, cost, sumsq, cnt);
+          associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, lvl_off,
+                                             lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
         }
       }
       // ---- deterministic group reduction in float64

@@ -363,7 +363,8 @@ extern "C" int rk_unproject_image(const rk_sensor* s, const float* range, int32_
 // (SURVEY Appendix A1).  One thread per pixel; neighbours come through L1.
 __global__ void __launch_bounds__(256) k_normals_cross(SensorDev s, const float* __restrict__ range,
                                                        int64_t total, float* normals,
-                                                       uint8_t* valid, float4* surfel) {
+                                                       uint8_t* valid, float4* surfel,
+                                                       int64_t surfel_pitch) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= total) return;
   const int W = s.W, H = s.H;
@@ -403,7 +404,22 @@ __global__ void __launch_bounds__(256) k_normals_cross(SensorDev s, const float*
     normals[3 * i + 2] = n2;
   }
   if (valid) valid[i] = ok ? 1 : 0;
-  if (surfel) surfel[i] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+  if (surfel) surfel[img * surfel_pitch + p] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+}
+
+// decimated copies of the full surfel maps (pixel (i, j) of level s = (i*s, j*s))
+__global__ void k_surfel_decimate(int H, int W, int batch, float4* pyr, int64_t pitch, int stride,
+                                  int64_t off) {
+  const int Hs = (H + stride - 1) / stride, Ws = (W + stride - 1) / stride;
+  const int64_t per = (int64_t)Hs * Ws, total = per * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t img = k / per;
+    const int q = (int)(k - img * per);
+    const int i = q / Ws, j = q - i * Ws;
+    float4* base = pyr + img * pitch;
+    base[off + q] = base[(int64_t)i * stride * W + (int64_t)j * stride];
+  }
 }
 
 extern "C" int rk_normals_cross(const rk_sensor* s, const float* range, int32_t batch,
@@ -411,8 +427,37 @@ extern "C" int rk_normals_cross(const rk_sensor* s, const float* range, int32_t 
   int64_t total = (int64_t)batch * s->dev.H * s->dev.W;
   if (total <= 0) return RK_OK;
   k_normals_cross<<<blocks_for(total, 256), 256, 0, S(stream)>>>(
-      s->dev, range, total, normals, valid, reinterpret_cast<float4*>(surfel));
+      s->dev, range, total, normals, valid, reinterpret_cast<float4*>(surfel),
+      (int64_t)s->dev.H * s->dev.W);
   RK_LAUNCHED("k_normals_cross");
+  return RK_OK;
+}
+
+extern "C" int rk_normals_cross_pyramid(const rk_sensor* s, const float* range, int32_t batch,
+                                        const int32_t* strides_host, int32_t n_strides,
+                                        float* surfel_pyr, int64_t pitch, void* stream) {
+  const int H = s->dev.H, W = s->dev.W;
+  const int64_t total = (int64_t)batch * H * W;
+  if (total <= 0) return RK_OK;
+  int64_t need = (int64_t)H * W;
+  for (int k = 0; k < n_strides; ++k) {
+    const int st = strides_host[k];
+    if (st < 1) { rk_set_error("strides must be >= 1"); return RK_EGENERIC; }
+    if (st > 1) need += (int64_t)((H + st - 1) / st) * ((W + st - 1) / st);
+  }
+  if (pitch < need) { rk_set_error("surfel pyramid pitch %lld < %lld", (long long)pitch, (long long)need); return RK_EGENERIC; }
+  float4* pyr = reinterpret_cast<float4*>(surfel_pyr);
+  k_normals_cross<<<blocks_for(total, 256), 256, 0, S(stream)>>>(s->dev, range, total, nullptr,
+                                                                  nullptr, pyr, pitch);
+  int64_t off = (int64_t)H * W;
+  for (int k = 0; k < n_strides; ++k) {
+    const int st = strides_host[k];
+    if (st <= 1) continue;
+    const int64_t per = (int64_t)((H + st - 1) / st) * ((W + st - 1) / st);
+    k_surfel_decimate<<<blocks_for(per * batch, 256), 256, 0, S(stream)>>>(H, W, batch, pyr, pitch, st, off);
+    off += per;
+  }
+  RK_LAUNCHED("rk_normals_cross_pyramid");
   return RK_OK;
 }
 

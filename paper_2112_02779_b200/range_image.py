@@ -312,13 +312,40 @@ def normals_cross(img: RangeImage) -> NormalImage:
     return NormalImage(nat.to_host(vec), nat.to_host(val).astype(bool), surf)
 
 
-def normals_cross_batch(intr: LidarIntrinsics, ranges):
-    """K1 over a (B, H, W) device batch -> (B, H, W, 4) surfel maps (batch API)."""
+@dataclass
+class SurfelPyramid:
+    """Per image: the full surfel map followed by the decimated map of every
+    coarse stride (rk_normals_cross_pyramid); ``offsets`` maps stride ->
+    pixel offset inside an image's ``pitch``-pixel block (stride 1 -> 0)."""
+
+    data: object
+    pitch: int
+    offsets: dict
+
+
+def normals_cross_batch(intr: LidarIntrinsics, ranges, strides=None):
+    """K1 over a (B, H, W) device batch -> (B, H, W, 4) surfel maps (batch
+    API), or with ``strides`` a SurfelPyramid whose coarse levels the
+    registration gathers from compact maps."""
     B = ranges.shape[0]
-    surf = nat.empty((B, intr.height, intr.width, 4), np.float32)
-    nat.call("rk_normals_cross", lm.device_sensor(intr), nat.ptr(ranges), B, None, None,
-             nat.ptr(surf), nat.stream_ptr())
-    return surf
+    H, W = intr.height, intr.width
+    if strides is None:
+        surf = nat.empty((B, H, W, 4), np.float32)
+        nat.call("rk_normals_cross", lm.device_sensor(intr), nat.ptr(ranges), B, None, None,
+                 nat.ptr(surf), nat.stream_ptr())
+        return surf
+    coarse = sorted({int(s) for s in strides if int(s) > 1})
+    offsets, off = {1: 0}, H * W
+    for s in coarse:
+        offsets[s] = off
+        off += -(-H // s) * -(-W // s)
+    pitch = off
+    data = nat.empty((B, pitch, 4), np.float32)
+    st = np.asarray(coarse, dtype=np.int32)
+    nat.call("rk_normals_cross_pyramid", lm.device_sensor(intr), nat.ptr(ranges), B,
+             st.ctypes.data if st.size else None, int(st.size), nat.ptr(data), int(pitch),
+             nat.stream_ptr())
+    return SurfelPyramid(data, pitch, offsets)
 
 
 @dataclass

@@ -19,7 +19,8 @@ import numpy as np
 from . import _native as nat
 from . import lidar_model as lm
 from .errors import DegenerateGeometry, EmptyInput, MissingNormals
-from .range_image import NormalImage, RangeImage, compute_normal_map, normals_cross_batch
+from .range_image import (NormalImage, RangeImage, SurfelPyramid, compute_normal_map,
+                          normals_cross_batch)
 from .se3 import RigidTransform
 
 DEFAULT_SCHEDULE = ((4, 20), (2, 20), (1, 10))
@@ -255,7 +256,8 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
 
     src_ranges / dst_ranges: (P, H, W) float32 CUDA tensors (image pools);
     pair_src / pair_dst: (B,) int32 indices into them (default: arange);
-    dst_surfels: (P, H, W, 4) from ``normals_cross_batch`` (computed if None);
+    dst_surfels: (P, H, W, 4) from ``normals_cross_batch`` or its SurfelPyramid
+    (coarse levels gather from compact decimated maps; computed if None);
     inits: (B, 12) float64 initial poses (default identity);
     pt_iters: optional (1,) int64 device counter of executed point-iterations.
     """
@@ -263,7 +265,7 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     src = src_ranges.contiguous()
     dst = dst_ranges.contiguous()
     if dst_surfels is None:
-        dst_surfels = normals_cross_batch(intr, dst)
+        dst_surfels = normals_cross_batch(intr, dst, strides=[s for s, _ in config.schedule])
     B = src.shape[0] if pair_src is None else pair_src.shape[0]
     dev = nat.device()
     if pair_src is None:
@@ -279,8 +281,17 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     max_it = config.max_iterations
     stats = t.empty((B, max_it, 5), dtype=t.float64, device=dev) if with_stats else None
     cfg = config.to_c(math)
+    surf = dst_surfels
+    if isinstance(dst_surfels, SurfelPyramid):
+        missing = [s for s, _ in config.schedule if int(s) not in dst_surfels.offsets]
+        if missing:
+            raise ValueError(f"surfel pyramid lacks strides {missing}")
+        cfg.surfel_pitch = int(dst_surfels.pitch)
+        for i, (s, _) in enumerate(config.schedule):
+            cfg.surfel_level_off[i] = int(dst_surfels.offsets[int(s)])
+        surf = dst_surfels.data
     nat.call("rk_register_batch", lm.device_sensor(intr), nat.ptr(src), nat.ptr(dst),
-             nat.ptr(dst_surfels), nat.ptr(pair_src.to(t.int32).contiguous()),
+             nat.ptr(surf), nat.ptr(pair_src.to(t.int32).contiguous()),
              nat.ptr(pair_dst.to(t.int32).contiguous()), B, nat.ptr(inits.contiguous()),
              C.byref(cfg), nat.ptr(poses), nat.ptr(status), nat.ptr(iters),
              nat.ptr(stats), max_it if with_stats else 0, nat.ptr(pt_iters), nat.stream_ptr())

@@ -267,6 +267,31 @@ def test_register_batch_deterministic_and_consistent(rk, sensors, golden_icp):
     assert np.array_equal(a.pose(0).matrix(), single.pose.matrix())
 
 
+@pytest.mark.parametrize("pair", PAIRS)
+def test_register_batch_surfel_pyramid_bitidentical(rk, pair, sensors, golden_icp):
+    """Coarse levels gathering from the decimated surfel maps see exactly the
+    values of the strided full-resolution reads: poses and iteration counts
+    are bit-identical (also for a sensor whose view width is not a multiple
+    of the CTA, i.e. the generic walk)."""
+    import torch
+    from paper_2112_02779_b200.range_image import SurfelPyramid, normals_cross_batch
+    g, intr = golden_icp, sensors[SENSOR_OF[pair]]
+    src = torch.from_numpy(g[f"{pair}/src"]).cuda()[None].repeat(3, 1, 1)
+    dst = torch.from_numpy(g[f"{pair}/dst"]).cuda()[None].repeat(3, 1, 1)
+    cfg = rk.RegistrationConfig(schedule=((4, 20), (3, 5), (2, 20), (1, 10)))
+    flat = normals_cross_batch(intr, dst)
+    pyr = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
+    assert isinstance(pyr, SurfelPyramid) and set(pyr.offsets) == {1, 2, 3, 4}
+    assert torch.equal(pyr.data[:, :intr.height * intr.width].reshape(flat.shape), flat)
+    a = rk.register_batch(intr, src, dst, flat, config=cfg, with_stats=True)
+    b = rk.register_batch(intr, src, dst, pyr, config=cfg, with_stats=True)
+    assert torch.equal(a.poses, b.poses) and torch.equal(a.iterations, b.iterations)
+    n = int(a.iterations[0])
+    assert torch.equal(a.stats[:, :n], b.stats[:, :n])
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, normals_cross_batch(intr, dst, strides=[4]), config=cfg)
+
+
 @pytest.mark.parametrize("wpp", ("1", "8"))
 def test_register_batch_layouts_match_reference(rk, wpp, sensors, golden_icp, monkeypatch):
     """Warp-per-pair and CTA-per-pair kernels both meet the reference contract."""
