@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
         float2 st = vox[i];
 #endif
         const float wn = __fadd_rn(st.y, 1.0f);
-        st.x = __fdiv_rn(__fadd_rn(__fmul_rn(st.y, st.x), d), wn);
+        // (w*tsdf + d) / (w + 1), correctly rounded (w + 1 in [1, max_weight + 1])
+        st.x = MATH == MATH_FAST ? div_rn_fast(__fadd_rn(__fmul_rn(st.y, st.x), d), wn)
+                                 : __fdiv_rn(__fadd_rn(__fmul_rn(st.y, st.x), d), wn);
         st.y = fminf(wn, A.max_w);
         vox[i] = st;
         ++count;
