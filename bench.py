@@ -247,12 +247,26 @@ def run_ours(args, rank, world, dist):
     upd_per_step = upd.item() / K
     tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd_per_step + TSDF_BYTES_PER_PIXEL * intr.height * intr.width * args.frames
     tsdf_achieved = tsdf_bytes / (acc["tsdf"] / K / 1e3) / 1e9
-    launches = K * (1 + 1 + pipeline.LAUNCHES_CLEAR + pipeline.LAUNCHES_PER_FRAME * args.frames)
+    coarse = len({s for s, _ in cfg.schedule if s > 1})
+    launches = K * (1 + coarse + 1 + pipeline.LAUNCHES_CLEAR + pipeline.LAUNCHES_PER_FRAME * args.frames)
+    mesh = None
+    if dist is None:
+        # K6 on the sequence's final grid (outside the timed region): one
+        # extract_mesh through the public API, wall clock incl. its syncs
+        from paper_2112_02779_b200.mesh_extract import extract_mesh_device
+        extract_mesh_device(grid)
+        torch.cuda.synchronize()
+        t_mc = time.perf_counter()
+        v, tri, _ = extract_mesh_device(grid)
+        torch.cuda.synchronize()
+        mesh = {"ms": 1e3 * (time.perf_counter() - t_mc), "vertices": int(v.shape[0]),
+                "triangles": int(tri.shape[0]), "blocks": int(n_blocks)}
     return dict(reg_per_s=reg_per_s, tsdf_fps=tsdf_fps, elapsed_ms=elapsed_ms, icp_ms=icp_ms,
                 tsdf_ms=tsdf_ms, achieved=achieved, pt_per_launch=pt_per_launch,
                 icp_kernel_ms=icp_kernel_ms, normals_ms=acc["normals"] / K,
                 tsdf_achieved=tsdf_achieved, tsdf_updated=upd_per_step, n_blocks=n_blocks,
-                clocks=clocks.summary(), launches=launches, ok_frac=ok_frac, D=D, tsdf=tsdf, cfg=cfg)
+                clocks=clocks.summary(), launches=launches, ok_frac=ok_frac, D=D, tsdf=tsdf, cfg=cfg,
+                mesh=mesh)
 
 
 def run_e2e(args, rank, world, dist, D, tsdf, cfg):
@@ -453,7 +467,9 @@ def main():
         "tsdf": {"value": r["tsdf_fps"], "unit": "frames/s", "voxels_updated_per_step": r["tsdf_updated"],
                  "blocks": r["n_blocks"],
                  "roofline": {"bound": "hbm", "achieved": r["tsdf_achieved"], "peak": peak, "unit": "GB/s",
-                              "frac": r["tsdf_achieved"] / peak, "traffic": profile_traffic("k_integrate")}},
+                              "frac": r["tsdf_achieved"] / peak,
+                              "traffic": (tt * r["tsdf_updated"] if (tt := profile_traffic("k_integrate"))
+                                          else None)}},
         "roofline": {"bound": "hbm", "kernel": "k_register", "achieved": r["achieved"], "peak": peak,
                      "unit": "GB/s", "frac": r["achieved"] / peak,
                      "traffic": (tr * r["pt_per_launch"] if tr else None),
@@ -462,6 +478,7 @@ def main():
         "phase_ms": {"normals": r["normals_ms"], "register": r["icp_kernel_ms"],
                      "tsdf_sequence": r["tsdf_ms"] / args.steps},
         "gt_recovered_frac": r["ok_frac"],
+        "marching_cubes": r["mesh"],
         "clocks": r["clocks"], "gpu_launches": r["launches"],
         "e2e": e2e, "cpu_baseline": cpu,
     }
