@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    # diagnostic only (not a bench configuration): every pair reads pool image 0's
+    # destination, isolating the cost of the data-dependent surfel gather
+    ap.add_argument("--diag-same-dst", action="store_true")
     return ap.parse_args()
 
 
@@ -127,7 +130,9 @@ def make_inputs(args, rank, world, device):
     inv_w = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).to(device)
     gts = np.stack([gt.as_row12() for _, gt in pool])
     torch.cuda.synchronize()
-    return dict(intr=intr, src=src, dst=dst, pair_idx=pair_idx, n_pairs=hi - lo, frames=frames,
+    pair_dst = torch.zeros_like(pair_idx) if args.diag_same_dst else pair_idx
+    return dict(intr=intr, src=src, dst=dst, pair_idx=pair_idx, pair_dst=pair_dst, n_pairs=hi - lo,
+                frames=frames,
                 poses_w=poses_w, inv_w=inv_w, traj=traj, gts=gts)
 
 
@@ -190,7 +195,7 @@ def run_ours(args, rank, world, dist):
         e[1].record(stream)
         ev["icp"][0].record(stream)
         res = rk.register_batch(intr, D["src"], D["dst"], surf, pair_src=D["pair_idx"],
-                                pair_dst=D["pair_idx"], config=cfg, pt_iters=pt_iters if timed else None)
+                                pair_dst=D["pair_dst"], config=cfg, pt_iters=pt_iters if timed else None)
         ev["icp"][1].record(stream)
         ev["tsdf"][0].record(stream)
         tsdf.run(D["frames"], D["poses_w"], D["inv_w"], updated if timed else updated_warm)
