@@ -34,7 +34,10 @@ static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p)
 namespace {
 
 constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
-constexpr int kThreads = 256;
+#ifndef RK_ICP_THREADS
+#define RK_ICP_THREADS 256
+#endif
+constexpr int kThreads = RK_ICP_THREADS;  // one CTA per pair by default (WPP = kThreads / 32)
 
 struct IcpArgs {
   SensorDev s;
@@ -580,20 +583,21 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   a.batch = batch;
   a.cfg = *cfg;
   a.pt_iters = pt_iters;
-  // CTA-per-pair (WPP = 8) measured fastest at every batch size on B200
-  // (profiles/README.md: 8 > 4 > 2 > 1 warps per pair at 16k pairs): fewer
-  // distinct pairs per SM keep each pair's surfel gathers L1/L2-local.
-  // RK_ICP_WPP=1|2|4 selects the other layouts for experiments.
+  // CTA-per-pair (WPP = 8 at 256 threads) measured fastest on B200 (DESIGN.md
+  // §3: 4 warps per pair -23%, 2 -25%): fewer distinct pairs per SM keep each
+  // pair's surfel gathers L1/L2-local.  RK_ICP_WPP=1|2|4 selects the other
+  // layouts for experiments.
   const char* force = getenv("RK_ICP_WPP");
-  const int wpp = force ? atoi(force) : 8;
+  const int wpp = force ? atoi(force) : kThreads / 32;
   cudaStream_t st = S(stream);
   constexpr int MINB = RK_ICP_MINB;
+  constexpr int WFULL = kThreads / 32;
   if (cfg->math == MATH_CR)
-    return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, 8, MINB>(a, st);
+    return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, WFULL, MINB>(a, st);
   switch (wpp) {
     case 1: return launch<MATH_FAST, 1, MINB>(a, st);
     case 2: return launch<MATH_FAST, 2, MINB>(a, st);
     case 4: return launch<MATH_FAST, 4, MINB>(a, st);
-    default: return launch<MATH_FAST, 8, MINB>(a, st);
+    default: return launch<MATH_FAST, WFULL, MINB>(a, st);
   }
 }
