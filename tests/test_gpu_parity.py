@@ -628,3 +628,19 @@ def test_sdfg_round_trip_bytes_and_values(rk, sensors, golden_tsdf, golden_next,
     with pytest.raises(rk.TruncatedPayload):
         (tmp_path / "short.sdfg").write_bytes(blob[:100])
         io_formats.read_grid(tmp_path / "short.sdfg")
+
+
+def test_register_single_plane_is_degenerate(rk, sensors, osensors):
+    """A single plane leaves three DoF unobservable: the reference raises
+    DegenerateGeometry (cond(H) > 1e12, registration.py:270-272); the
+    warp-parallel update must route it to the exact test and agree."""
+    import torch
+    from oracle import synth as osynth
+    intr = sensors["small"]
+    img = osynth.render(osensors["small"], [("plane", (1.0, 0.0, 0.0), -4.0)])
+    assert (img > 0).sum() > 1000
+    with pytest.raises(rk.DegenerateGeometry):
+        rk.register(rk.RangeImage(img, intr), rk.RangeImage(img, intr))
+    t = torch.from_numpy(img).cuda()[None].repeat(2, 1, 1)
+    res = rk.register_batch(intr, t, t)
+    assert res.status.tolist() == [2, 2]
