@@ -239,6 +239,19 @@ int rk_grid_integrate_frames(rk_grid* g, const rk_sensor* s, const float* frames
                              const double* poses12, const double* invs12, double radius,
                              float clip_min, float clip_max, int math, int64_t* updated,
                              void* stream);
+/* Batched form of the sharded sequence: activate F frames into touched-set
+ * slots 0..F-1 (rk_grid_reserve_slots(g, F) first), export their {count, max
+ * key} pairs (F,2), all-reduce them across ranks in ONE collective (sum,
+ * max), then integrate all F frames with those global pairs (NULL = local). */
+int rk_grid_reserve_slots(rk_grid* g, int32_t n, void* stream);
+int rk_grid_activate_frames(rk_grid* g, const rk_sensor* s, const float* frames, int32_t n_frames,
+                            const double* poses12, double radius, float clip_min, float clip_max,
+                            void* stream);
+int rk_grid_touch_stats_frames(rk_grid* g, int32_t n_frames, int64_t* out2n, void* stream);
+int rk_grid_integrate_activated(rk_grid* g, const rk_sensor* s, const float* frames,
+                                int32_t n_frames, const double* invs12, const int64_t* global2n,
+                                float clip_min, float clip_max, int math, int64_t* updated,
+                                void* stream);
 /* multi-GPU hash sharding: the grid only allocates blocks whose
  * owner(key) == rank; rk_block_owner is the host mirror of owner() for
  * keys_host (n,3).  Sharded integration needs the frame's global touched

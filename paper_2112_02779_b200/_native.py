@@ -83,6 +83,10 @@ SIGNATURES = {
     "rk_grid_set_touched": [_p, _p, _i64, _p],
     "rk_grid_integrate": [_p, _p, _p, _p, _f32, _f32, C.c_int, _p, _p],
     "rk_grid_integrate_frames": [_p, _p, _p, _i32, _p, _p, _f64, _f32, _f32, C.c_int, _p, _p],
+    "rk_grid_reserve_slots": [_p, _i32, _p],
+    "rk_grid_activate_frames": [_p, _p, _p, _i32, _p, _f64, _f32, _f32, _p],
+    "rk_grid_touch_stats_frames": [_p, _i32, _p, _p],
+    "rk_grid_integrate_activated": [_p, _p, _p, _i32, _p, _p, _f32, _f32, C.c_int, _p, _p],
     "rk_grid_keys": [_p, C.c_int, _p, _i64, _p, _p],
     "rk_grid_read_blocks": [_p, _p, _i64, _p, _p, _p],
     "rk_grid_write_blocks": [_p, _p, _i64, _p, _p],

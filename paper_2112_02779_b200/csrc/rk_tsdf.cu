@@ -585,6 +585,7 @@ struct rk_grid {
   GridDev d;              // slot-0 view; d.touched / d.tc are the bases of both slots
   unsigned long long hash_cap;
   int last_slot = 0;      // touched-set slot of the most recent activation
+  int n_slots = 2;        // touched-set slots (>= 2; rk_grid_reserve_slots grows them)
   const long long* global_touch = nullptr;  // device {count, max key} (sharded grids)
   cudaStream_t side = nullptr;               // activation stream of rk_grid_integrate_frames
   cudaEvent_t ev_act[2] = {nullptr, nullptr}, ev_int[2] = {nullptr, nullptr}, ev_fork = nullptr;
@@ -634,7 +635,7 @@ static int alloc_tables(rk_grid* g, long long cap_blocks, cudaStream_t st) {
   RK_CUDA(cudaMemsetAsync(d.h_slot, 0xff, hcap * sizeof(int32_t), st));
   RK_CUDA(cudaMalloc(&d.h_stamp, hcap * sizeof(int32_t)));
   RK_CUDA(cudaMemsetAsync(d.h_stamp, 0, hcap * sizeof(int32_t), st));
-  RK_CUDA(cudaMalloc(&d.touched, 2 * hcap * sizeof(int32_t)));  // two touched-set slots
+  RK_CUDA(cudaMalloc(&d.touched, (size_t)g->n_slots * hcap * sizeof(int32_t)));  // touched-set slots
   RK_CUDA(cudaMalloc(&d.fresh, hcap * sizeof(int32_t)));
   d.cap_blocks = cap_blocks;
   d.hash_mask = hcap - 1;
@@ -668,10 +669,10 @@ extern "C" int rk_grid_create(double voxel_size, double truncation, float max_we
   if (capacity_blocks < 64) capacity_blocks = 64;
   int rc = alloc_tables(g, capacity_blocks, 0);
   if (rc) { delete g; return rc; }
-  // counters and the two touched-set slots' counters in one allocation
-  RK_CUDA(cudaMalloc(&g->d.ctr, sizeof(Counters) + 2 * sizeof(TouchCounters)));
-  RK_CUDA(cudaMemset(g->d.ctr, 0, sizeof(Counters) + 2 * sizeof(TouchCounters)));
-  g->d.tc = reinterpret_cast<TouchCounters*>(g->d.ctr + 1);
+  RK_CUDA(cudaMalloc(&g->d.ctr, sizeof(Counters)));
+  RK_CUDA(cudaMemset(g->d.ctr, 0, sizeof(Counters)));
+  RK_CUDA(cudaMalloc(&g->d.tc, g->n_slots * sizeof(TouchCounters)));
+  RK_CUDA(cudaMemset(g->d.tc, 0, g->n_slots * sizeof(TouchCounters)));
   RK_CUDA(set_integrate_attrs());
   // side stream + events of rk_grid_integrate_frames, created here so that the
   // sequence call itself can run under stream capture
@@ -691,6 +692,7 @@ extern "C" int rk_grid_destroy(rk_grid* g) {
   cudaDeviceSynchronize();
   free_tables(g->d);
   cudaFree(g->d.ctr);
+  cudaFree(g->d.tc);
   if (g->side) {
     cudaStreamDestroy(g->side);
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(g->ev_act[i]); cudaEventDestroy(g->ev_int[i]); }
@@ -721,7 +723,7 @@ extern "C" int rk_grid_reserve(rk_grid* g, int64_t capacity_blocks, void* stream
   c.overflow = 0;
   c.n_fresh = 0;
   RK_CUDA(cudaMemcpyAsync(g->d.ctr, &c, sizeof(c), cudaMemcpyHostToDevice, st));
-  RK_CUDA(cudaMemsetAsync(g->d.tc, 0, 2 * sizeof(TouchCounters), st));
+  RK_CUDA(cudaMemsetAsync(g->d.tc, 0, g->n_slots * sizeof(TouchCounters), st));
   RK_CUDA(cudaStreamSynchronize(st));
   free_tables(old);
   return RK_OK;
@@ -789,7 +791,7 @@ extern "C" int rk_grid_set_touched(rk_grid* g, const int32_t* keys, int64_t n, v
 
 static int integrate_slot(rk_grid* g, const rk_sensor* s, const float* range, const double* inv12,
                           float clip_min, float clip_max, int math, int64_t* updated, int slot,
-                          cudaStream_t st) {
+                          cudaStream_t st, const long long* global_touch) {
   IntegrateArgs a;
   a.g = view(g, slot);
   a.s = s->dev;
@@ -803,7 +805,7 @@ static int integrate_slot(rk_grid* g, const rk_sensor* s, const float* range, co
   a.cmax = clip_max;
   a.free_space = g->free_space;
   a.updated = reinterpret_cast<long long*>(updated);
-  a.global_touch = g->global_touch;
+  a.global_touch = global_touch;
   constexpr int NT = kIntegrateThreads;
   const unsigned grid = (unsigned)(num_sms() * kIntegrateCtasPerSm);
   const size_t smem = kLatticeBytes;
@@ -822,7 +824,7 @@ extern "C" int rk_grid_integrate(rk_grid* g, const rk_sensor* s, const float* ra
                                  const double* inv12, float clip_min, float clip_max, int math,
                                  int64_t* updated, void* stream) {
   return integrate_slot(g, s, range, inv12, clip_min, clip_max, math, updated, g->last_slot,
-                        S(stream));
+                        S(stream), g->global_touch);
 }
 
 // F frames: activation of frame f+1 (side stream) overlaps the integration of
@@ -848,7 +850,7 @@ extern "C" int rk_grid_integrate_frames(rk_grid* g, const rk_sensor* s, const fl
     RK_CUDA(cudaEventRecord(g->ev_act[slot], g->side));
     RK_CUDA(cudaStreamWaitEvent(st, g->ev_act[slot], 0));
     rc = integrate_slot(g, s, frames + f * px, invs12 + 12 * f, clip_min, clip_max, math, updated,
-                        slot, st);
+                        slot, st, nullptr);
     if (rc) return rc;
     RK_CUDA(cudaEventRecord(g->ev_int[slot], st));
   }
@@ -857,6 +859,75 @@ extern "C" int rk_grid_integrate_frames(rk_grid* g, const rk_sensor* s, const fl
   RK_CUDA(cudaEventRecord(g->ev_act[0], g->side));
   RK_CUDA(cudaStreamWaitEvent(st, g->ev_act[0], 0));
   g->last_slot = (n_frames - 1) & 1;
+  return RK_OK;
+}
+
+// ---- batched activation for hash-sharded multi-GPU grids: all F frames are
+// activated first (one touched-set slot each), their {count, max key} pairs
+// reduced across ranks in ONE collective, then all F frames integrated.
+extern "C" int rk_grid_reserve_slots(rk_grid* g, int32_t n, void* stream) {
+  if (n <= g->n_slots) return RK_OK;
+  cudaStream_t st = S(stream);
+  RK_CUDA(cudaStreamSynchronize(st));
+  int32_t* touched = nullptr;
+  TouchCounters* tc = nullptr;
+  RK_CUDA(cudaMalloc(&touched, (size_t)n * g->hash_cap * sizeof(int32_t)));
+  RK_CUDA(cudaMalloc(&tc, n * sizeof(TouchCounters)));
+  RK_CUDA(cudaMemset(tc, 0, n * sizeof(TouchCounters)));
+  RK_CUDA(cudaMemcpy(touched, g->d.touched, (size_t)g->n_slots * g->hash_cap * sizeof(int32_t),
+                     cudaMemcpyDeviceToDevice));
+  RK_CUDA(cudaMemcpy(tc, g->d.tc, g->n_slots * sizeof(TouchCounters), cudaMemcpyDeviceToDevice));
+  cudaFree(g->d.touched);
+  cudaFree(g->d.tc);
+  g->d.touched = touched;
+  g->d.tc = tc;
+  g->n_slots = n;
+  return RK_OK;
+}
+
+extern "C" int rk_grid_activate_frames(rk_grid* g, const rk_sensor* s, const float* frames,
+                                       int32_t n_frames, const double* poses12, double radius,
+                                       float clip_min, float clip_max, void* stream) {
+  if (n_frames > g->n_slots) {
+    rk_set_error("%d frames need rk_grid_reserve_slots (have %d slots)", n_frames, g->n_slots);
+    return RK_EGENERIC;
+  }
+  const size_t px = (size_t)s->dev.H * s->dev.W;
+  for (int f = 0; f < n_frames; ++f) {
+    const int rc = activate_image_slot(g, s, frames + f * px, poses12 + 12 * f, radius, clip_min,
+                                       clip_max, f, S(stream));
+    if (rc) return rc;
+  }
+  g->last_slot = n_frames > 0 ? n_frames - 1 : 0;
+  return RK_OK;
+}
+
+__global__ void k_touch_stats_frames(const TouchCounters* t, int n, long long* out) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  out[2 * f] = t[f].n_touched;
+  out[2 * f + 1] = (long long)t[f].max_touched_key;
+}
+
+extern "C" int rk_grid_touch_stats_frames(rk_grid* g, int32_t n_frames, int64_t* out2n, void* stream) {
+  if (n_frames <= 0) return RK_OK;
+  k_touch_stats_frames<<<(n_frames + 127) / 128, 128, 0, S(stream)>>>(
+      g->d.tc, n_frames, reinterpret_cast<long long*>(out2n));
+  RK_LAUNCHED("k_touch_stats_frames");
+  return RK_OK;
+}
+
+extern "C" int rk_grid_integrate_activated(rk_grid* g, const rk_sensor* s, const float* frames,
+                                           int32_t n_frames, const double* invs12,
+                                           const int64_t* global2n, float clip_min, float clip_max,
+                                           int math, int64_t* updated, void* stream) {
+  const size_t px = (size_t)s->dev.H * s->dev.W;
+  const long long* glob = reinterpret_cast<const long long*>(global2n);
+  for (int f = 0; f < n_frames; ++f) {
+    const int rc = integrate_slot(g, s, frames + f * px, invs12 + 12 * f, clip_min, clip_max, math,
+                                  updated, f, S(stream), glob ? glob + 2 * f : nullptr);
+    if (rc) return rc;
+  }
   return RK_OK;
 }
 
@@ -931,13 +1002,13 @@ __global__ void k_clear_blocks(GridDev g) {
        i += (long long)gridDim.x * blockDim.x)
     v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
-__global__ void k_clear_counters(Counters* c, TouchCounters* t) {
+__global__ void k_clear_counters(Counters* c, TouchCounters* t, int n_slots) {
   c->n_blocks = 0;
   c->n_fresh = 0;
   c->overflow = 0;
   c->updated = 0;
   c->n_points = 0;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < n_slots; ++i) {
     t[i].n_touched = 0;
     t[i].max_touched_key = 0ull;
   }
@@ -950,7 +1021,7 @@ extern "C" int rk_grid_clear(rk_grid* g, void* stream) {
   k_clear_blocks<<<148 * 8, 256, 0, st>>>(g->d);
   RK_CUDA(cudaMemsetAsync(g->d.h_keys, 0xff, g->hash_cap * sizeof(unsigned long long), st));
   RK_CUDA(cudaMemsetAsync(g->d.h_slot, 0xff, g->hash_cap * sizeof(int32_t), st));
-  k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr, g->d.tc);
+  k_clear_counters<<<1, 1, 0, st>>>(g->d.ctr, g->d.tc, g->n_slots);
   RK_LAUNCHED("rk_grid_clear");
   return RK_OK;
 }

@@ -90,6 +90,18 @@ def reduce_touch_stats(stats, dist=None):
     return stats
 
 
+def reduce_touch_stats_frames(stats, dist=None):
+    """(F, 2) per-frame {local count, local max key} -> global {sum, max}
+    with one all-gather for the whole sequence (returns a new tensor)."""
+    import torch
+    import torch.distributed as tdist
+    d = dist or tdist
+    bufs = [torch.empty_like(stats) for _ in range(d.get_world_size())]
+    d.all_gather(bufs, stats.contiguous())
+    allv = torch.stack(bufs)                     # (world, F, 2)
+    return torch.stack([allv[..., 0].sum(0), allv[..., 1].max(0).values], -1).contiguous()
+
+
 def block_owner(keys, world: int) -> np.ndarray:
     """Owning rank of each block key (host mirror of the device owner hash)."""
     k = np.ascontiguousarray(np.asarray(keys, dtype=np.int32).reshape(-1, 3))
@@ -106,14 +118,16 @@ class ShardedGrid:
         self.grid = VoxelBlockGrid(voxel_size=voxel_size, **grid_kw)
         self.rank, self.world, self.dist = rank, world, dist
         nat.call("rk_grid_set_shard", self.grid._ensure(), int(rank), int(world))
-        self._touch = nat.zeros((2,), np.int64)
-        if world > 1:
-            nat.call("rk_grid_set_global_touch", self.grid._handle, nat.ptr(self._touch))
 
     def integrate_frames(self, intr, frames, poses_w, inv_w, clip_min=0.0, clip_max=np.inf,
                          updated=None):
         """integrate_cloud_frame for F frames on this rank's shard.  frames /
-        poses must already be identical on every rank (see broadcast_frames)."""
+        poses must already be identical on every rank (see broadcast_frames).
+
+        All F frames are activated first (one touched-set slot each), the
+        per-frame {count, max key} pairs are reduced across ranks in one
+        collective (the reference's sorted-chunk arithmetic needs the global
+        values), then the F integrations run back to back."""
         from . import lidar_model as lm
         g = self.grid
         h = g._prepare()
@@ -121,15 +135,19 @@ class ShardedGrid:
         if updated is None:
             updated = nat.zeros((1,), np.int64)
         st = nat.stream_ptr()
+        F = int(frames.shape[0])
         cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
-        for f in range(frames.shape[0]):
-            nat.call("rk_grid_activate_image", h, sensor, nat.ptr(frames[f]), nat.ptr(poses_w[f]),
-                     float(g.truncation), cmin, cmax, st)
-            if self.world > 1:
-                nat.call("rk_grid_touch_stats", h, nat.ptr(self._touch), st)
-                reduce_touch_stats(self._touch, self.dist)
-            nat.call("rk_grid_integrate", h, sensor, nat.ptr(frames[f]), nat.ptr(inv_w[f]), cmin, cmax,
-                     lm.default_math(), nat.ptr(updated), st)
+        frames, poses_w, inv_w = frames.contiguous(), poses_w.contiguous(), inv_w.contiguous()
+        nat.call("rk_grid_reserve_slots", h, F, st)
+        nat.call("rk_grid_activate_frames", h, sensor, nat.ptr(frames), F, nat.ptr(poses_w),
+                 float(g.truncation), cmin, cmax, st)
+        glob = None
+        if self.world > 1:
+            stats = nat.zeros((F, 2), np.int64)
+            nat.call("rk_grid_touch_stats_frames", h, F, nat.ptr(stats), st)
+            glob = reduce_touch_stats_frames(stats, self.dist)
+        nat.call("rk_grid_integrate_activated", h, sensor, nat.ptr(frames), F, nat.ptr(inv_w),
+                 nat.ptr(glob), cmin, cmax, lm.default_math(), nat.ptr(updated), st)
         g.blocks._bump()
         return updated
 

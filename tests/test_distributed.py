@@ -71,6 +71,11 @@ def _touch_job(rank, world):
     return stats.tolist()
 
 
+def _touch_frames_job(rank, world):
+    stats = torch.tensor([[10 + rank, 1000 * (rank + 1)], [5, 7 - rank], [0, 0]], dtype=torch.int64)
+    return rkd.reduce_touch_stats_frames(stats).tolist()
+
+
 def _pair_shard_job(rank, world):
     """Each rank 'registers' its slice (a stand-in transform of the pair id);
     the gathered poses must equal the single-rank result in order."""
@@ -105,6 +110,12 @@ def test_broadcast_frames_gloo():
 def test_reduce_touch_stats_gloo():
     out = run_ranks(_touch_job)
     assert out[0] == out[1] == [21, 2000]
+
+
+def test_reduce_touch_stats_frames_gloo():
+    """The batched sharded sequence reduces all F frames' pairs in one collective."""
+    out = run_ranks(_touch_frames_job)
+    assert out[0] == out[1] == [[21, 2000], [10, 7], [0, 0]]
 
 
 def test_sharded_pairs_gather_in_order_gloo():

@@ -488,6 +488,51 @@ def test_hash_sharded_grid_equals_single_grid(rk, sensors, golden_icp):
             assert np.array_equal(b.tsdf, fb[k].tsdf) and np.array_equal(b.weight, fb[k].weight)
 
 
+def test_sharded_batched_sequence_equals_single_grid(rk, sensors):
+    """The multi-GPU TSDF flow (ShardedGrid.integrate_frames: F activations
+    into F slots, one reduction of the per-frame {count, max key}, F
+    integrations), emulated with two shards in one process, reproduces the
+    unsharded sequence bit for bit."""
+    import torch
+    from paper_2112_02779_b200 import _native as nat
+    from paper_2112_02779_b200 import lidar_model as lm
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = sensors["ouster"]
+    traj = scenes.street_trajectory(5, seed=0)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    poses = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    inv = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).cuda()
+    full = rk.VoxelBlockGrid(voxel_size=0.05, capacity=8192)
+    n_full = pipeline.integrate_sequence(full, intr, frames, poses, inv, clip_max=30.0)
+    F, st = frames.shape[0], nat.stream_ptr()
+    sensor = lm.device_sensor(intr)
+    shards = [rk.VoxelBlockGrid(voxel_size=0.05, capacity=8192) for _ in range(2)]
+    stats = []
+    for r, g in enumerate(shards):
+        h = g._ensure()
+        nat.call("rk_grid_set_shard", h, r, 2)
+        nat.call("rk_grid_reserve_slots", h, F, st)
+        nat.call("rk_grid_activate_frames", h, sensor, nat.ptr(frames), F, nat.ptr(poses),
+                 float(g.truncation), 0.0, 30.0, st)
+        s2 = nat.zeros((F, 2), np.int64)
+        nat.call("rk_grid_touch_stats_frames", h, F, nat.ptr(s2), st)
+        stats.append(s2)
+    glob = torch.stack([stats[0][:, 0] + stats[1][:, 0], torch.maximum(stats[0][:, 1], stats[1][:, 1])],
+                       -1).contiguous()
+    upd = nat.zeros((1,), np.int64)
+    for g in shards:
+        nat.call("rk_grid_integrate_activated", g._handle, sensor, nat.ptr(frames), F, nat.ptr(inv),
+                 nat.ptr(glob), 0.0, 30.0, lm.default_math(), nat.ptr(upd), st)
+        g.blocks._bump()
+    assert int(upd.item()) == int(n_full.item())
+    kf, vf = full.export_blocks()
+    parts = [g.export_blocks() for g in shards]
+    k = np.concatenate([p[0] for p in parts])
+    v = np.concatenate([p[1] for p in parts])
+    order = np.lexsort((k[:, 2], k[:, 1], k[:, 0]))
+    assert np.array_equal(k[order], kf) and np.array_equal(v[order], vf)
+
+
 def test_integrate_rejects_bad_pose(rk, sensors, golden_icp):
     grid = rk.VoxelBlockGrid(voxel_size=0.1)
     img = rk.RangeImage(golden_icp["synth/dst"], sensors["synth"])
