@@ -403,13 +403,30 @@ def measured_peak():
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def profile_traffic(kernel: str):
-    """dram bytes per work unit from the committed ncu capture, if any."""
+def profile_traffic(kernel: str, key: str | None = None):
+    """dram bytes (or, with key="instructions", warp instructions) per work
+    unit from the committed ncu captures (profiles/traffic.json), if any."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get(kernel)
+        return d.get(key, {}).get(kernel) if key else d.get(kernel)
     return None
+
+
+def issue_roofline(kernel: str, units: float, seconds: float, sm_mhz):
+    """The bound these kernels actually sit on: warp-instruction issue.  Peak =
+    4 schedulers x SMs x SM clock (one warp instruction per scheduler per
+    cycle); instructions per unit from the committed ncu capture."""
+    ipu = profile_traffic(kernel, "instructions")
+    if not ipu or not seconds:
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    clk = (sm_mhz or 1965.0) * 1e6
+    achieved = ipu * units / seconds
+    peak = 4 * sms * clk
+    return {"bound": "issue", "unit": "warp-instr/s", "instr_per_unit": ipu, "achieved": achieved,
+            "peak": peak, "frac": achieved / peak, "sm_mhz": clk / 1e6}
 
 
 def dist_init(args):
@@ -480,6 +497,11 @@ def main():
                      "traffic": (tr * r["pt_per_launch"] if tr else None),
                      "work": f"{r['pt_per_launch']:.4g} source-point-iterations x {ICP_BYTES_PER_PT_IT} B "
                              f"per launch, {r['icp_kernel_ms']:.2f} ms/launch", "peak_source": peak_src},
+        "issue_roofline": {
+            "k_register": issue_roofline("k_register", r["pt_per_launch"], r["icp_kernel_ms"] / 1e3,
+                                         r["clocks"].get("sm_mhz")),
+            "k_integrate": issue_roofline("k_integrate", r["tsdf_updated"],
+                                          r["tsdf_ms"] / args.steps / 1e3, r["clocks"].get("sm_mhz"))},
         "phase_ms": {"normals": r["normals_ms"], "register": r["icp_kernel_ms"],
                      "tsdf_sequence": r["tsdf_ms"] / args.steps},
         "gt_recovered_frac": r["ok_frac"],

@@ -1,15 +1,12 @@
-// rk_icp.cu -- K3: projective association + point-to-plane normal equations +
-// per-pair Gauss-Newton update, the whole multi-scale schedule in one launch.
-//
-// Layout: one CTA per registration pair (persistent over all levels and
-// iterations; the pose lives in shared memory).  Each iteration every thread
-// walks a row-major slice of the stride-s source view straight out of the
-// zero-copy level-0 image (the "pyramid" is index arithmetic, as in the
-// reference's StridedView), accumulates the 21+6 normal-equation terms in
-// float32 registers (the reference's sgemm precision), and the CTA reduces
-// them in float64 with a fixed shuffle/shared-memory tree -- deterministic,
-// no float atomics.  Thread 0 then solves the 6x6 system, applies the twist,
-// and decides the level's early exit (registration.py:261-282).
+// rk_icp.cu -- the per-call registration API around K3 (the batched
+// multi-scale kernel itself lives in rk_register.cu):
+//  * projective_correspondences(single=True) for an explicit float64 cloud
+//    (registration.py:117-187), bit-exact float32 association;
+//  * the float64 path's association given rk_project_f64 output (single=False);
+//  * float64 robust normal equations, point-to-plane residuals and centroid
+//    translation (registration.py:96-102, 190-234) with fixed-order block
+//    partials -- deterministic, no float atomics;
+//  * surfel maps from an explicit NormalImage.
 #include "rk_common.cuh"
 #include "rk_linalg.cuh"
 
