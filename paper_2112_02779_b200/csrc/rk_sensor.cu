@@ -360,51 +360,91 @@ extern "C" int rk_unproject_image(const rk_sensor* s, const float* range, int32_
 }
 
 // K1: cross-product normals (range_image.py:221-240) in the pinned op order
-// (SURVEY Appendix A1).  One thread per pixel; neighbours come through L1.
-__global__ void __launch_bounds__(256) k_normals_cross(SensorDev s, const float* __restrict__ range,
-                                                       int64_t total, float* normals,
-                                                       uint8_t* valid, float4* surfel,
-                                                       int64_t surfel_pitch) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= total) return;
+// (SURVEY Appendix A1).  A CTA owns a K1_TH x K1_TW tile of one image and
+// unprojects each pixel of the tile plus its right/down halo ONCE into shared
+// memory (a per-pixel kernel would unproject every point three times).
+constexpr int K1_TW = 128, K1_TH = 8, K1_THREADS = 256;
+__global__ void __launch_bounds__(K1_THREADS) k_normals_cross(
+    SensorDev s, const float* __restrict__ range, int batch, float* normals, uint8_t* valid,
+    float4* surfel, int64_t surfel_pitch) {
+  constexpr int PW = K1_TW + 1, PH = K1_TH + 1;
+  __shared__ double sp[3][PH * PW];
+  __shared__ float sr[PH * PW];
   const int W = s.W, H = s.H;
+  const int tiles_x = (W + K1_TW - 1) / K1_TW, tiles_y = (H + K1_TH - 1) / K1_TH;
   const int64_t HW = (int64_t)H * W;
-  const int64_t img = i / HW;
-  const int p = (int)(i - img * HW);
-  const int v = p / W, u = p - v * W;
+  const int t = blockIdx.x;
+  const int img = t / (tiles_x * tiles_y);
+  const int tt = t - img * (tiles_x * tiles_y);
+  const int v0 = (tt / tiles_x) * K1_TH, u0 = (tt - (tt / tiles_x) * tiles_x) * K1_TW;
   const float* R = range + img * HW;
-  const float r0 = R[p];
-  const int ur = (u + 1 == W) ? 0 : u + 1;
-  const float rr = R[v * W + ur];
-  const bool has_down = v + 1 < H;
-  const float rd = has_down ? R[(v + 1) * W + u] : 0.f;
-  bool ok = r0 > 0.f && rr > 0.f && has_down && rd > 0.f;
-  double P[3], Pr[3], Pd[3];
-  unproject_px(s, v, u, r0, P);
-  unproject_px(s, v, ur, rr, Pr);
-  if (has_down) unproject_px(s, v + 1, u, rd, Pd);
-  else Pd[0] = Pd[1] = Pd[2] = 0.0;
-  double a0 = __dsub_rn(Pr[0], P[0]), a1 = __dsub_rn(Pr[1], P[1]), a2 = __dsub_rn(Pr[2], P[2]);
-  double b0 = __dsub_rn(Pd[0], P[0]), b1 = __dsub_rn(Pd[1], P[1]), b2 = __dsub_rn(Pd[2], P[2]);
-  double c0 = __dsub_rn(__dmul_rn(a1, b2), __dmul_rn(a2, b1));
-  double c1 = __dsub_rn(__dmul_rn(a2, b0), __dmul_rn(a0, b2));
-  double c2 = __dsub_rn(__dmul_rn(a0, b1), __dmul_rn(a1, b0));
-  double nn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(c0, c0), __dmul_rn(c1, c1)), __dmul_rn(c2, c2)));
-  ok = ok && nn > 1e-12;
-  float n0 = 0.f, n1 = 0.f, n2 = 0.f;
-  if (ok) {
-    double m0 = __ddiv_rn(c0, nn), m1 = __ddiv_rn(c1, nn), m2 = __ddiv_rn(c2, nn);
-    double facing = __dadd_rn(__dadd_rn(__dmul_rn(m0, P[0]), __dmul_rn(m1, P[1])), __dmul_rn(m2, P[2]));
-    if (facing > 0.0) { m0 = -m0; m1 = -m1; m2 = -m2; }
-    n0 = (float)m0; n1 = (float)m1; n2 = (float)m2;
+  for (int k = threadIdx.x; k < PH * PW; k += K1_THREADS) {
+    const int dv = k / PW, du = k - dv * PW;
+    const int v = v0 + dv;
+    int u = u0 + du;
+    if (u >= W) u -= W;  // azimuth wrap (the halo of the last tile is column 0)
+    float r = 0.0f;
+    double P[3] = {0.0, 0.0, 0.0};
+    if (v < H) {
+      r = __ldg(R + (int64_t)v * W + u);
+      unproject_px(s, v, u, r, P);
+    }
+    sr[k] = r;
+    sp[0][k] = P[0];
+    sp[1][k] = P[1];
+    sp[2][k] = P[2];
   }
-  if (normals) {
-    normals[3 * i] = n0;
-    normals[3 * i + 1] = n1;
-    normals[3 * i + 2] = n2;
+  __syncthreads();
+  for (int k = threadIdx.x; k < K1_TH * K1_TW; k += K1_THREADS) {
+    const int dv = k / K1_TW, du = k - dv * K1_TW;
+    const int v = v0 + dv, u = u0 + du;
+    if (v >= H || u >= W) continue;
+    const int c = dv * PW + du, cr = c + 1, cd = c + PW;
+    const float r0 = sr[c];
+    const bool has_down = v + 1 < H;
+    const bool ok0 = r0 > 0.f && sr[cr] > 0.f && has_down && sr[cd] > 0.f;
+    const double P0 = sp[0][c], P1 = sp[1][c], P2 = sp[2][c];
+    const double a0 = __dsub_rn(sp[0][cr], P0), a1 = __dsub_rn(sp[1][cr], P1), a2 = __dsub_rn(sp[2][cr], P2);
+    // the reference's "down" row below the image is 0.0 (range_image.py:227-228)
+    const double d0 = has_down ? sp[0][cd] : 0.0, d1 = has_down ? sp[1][cd] : 0.0,
+                 d2 = has_down ? sp[2][cd] : 0.0;
+    const double b0 = __dsub_rn(d0, P0), b1 = __dsub_rn(d1, P1), b2 = __dsub_rn(d2, P2);
+    const double c0 = __dsub_rn(__dmul_rn(a1, b2), __dmul_rn(a2, b1));
+    const double c1 = __dsub_rn(__dmul_rn(a2, b0), __dmul_rn(a0, b2));
+    const double c2 = __dsub_rn(__dmul_rn(a0, b1), __dmul_rn(a1, b0));
+    const double nn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(c0, c0), __dmul_rn(c1, c1)), __dmul_rn(c2, c2)));
+    const bool ok = ok0 && nn > 1e-12;
+    float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+    if (ok) {
+      // c / nn correctly rounded: y = RN(1/nn), q = RN(c*y) plus one residual
+      // correction (Markstein; exact for normal operands, |c| <= nn here)
+      const double y = __drcp_rn(nn);
+      double m0 = __dmul_rn(c0, y), m1 = __dmul_rn(c1, y), m2 = __dmul_rn(c2, y);
+      m0 = __fma_rn(__fma_rn(-nn, m0, c0), y, m0);
+      m1 = __fma_rn(__fma_rn(-nn, m1, c1), y, m1);
+      m2 = __fma_rn(__fma_rn(-nn, m2, c2), y, m2);
+      const double facing = __dadd_rn(__dadd_rn(__dmul_rn(m0, P0), __dmul_rn(m1, P1)), __dmul_rn(m2, P2));
+      if (facing > 0.0) { m0 = -m0; m1 = -m1; m2 = -m2; }
+      n0 = (float)m0; n1 = (float)m1; n2 = (float)m2;
+    }
+    const int64_t p = (int64_t)v * W + u;
+    const int64_t i = img * HW + p;
+    if (normals) {
+      normals[3 * i] = n0;
+      normals[3 * i + 1] = n1;
+      normals[3 * i + 2] = n2;
+    }
+    if (valid) valid[i] = ok ? 1 : 0;
+    if (surfel) surfel[img * surfel_pitch + p] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
   }
-  if (valid) valid[i] = ok ? 1 : 0;
-  if (surfel) surfel[img * surfel_pitch + p] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+}
+
+static void launch_k1(const rk_sensor* s, const float* range, int32_t batch, float* normals,
+                      uint8_t* valid, float4* surfel, int64_t pitch, cudaStream_t st) {
+  const int W = s->dev.W, H = s->dev.H;
+  const unsigned tiles = (unsigned)(((W + K1_TW - 1) / K1_TW) * ((H + K1_TH - 1) / K1_TH));
+  k_normals_cross<<<tiles * (unsigned)batch, K1_THREADS, 0, st>>>(s->dev, range, batch, normals,
+                                                                  valid, surfel, pitch);
 }
 
 // decimated copies of the full surfel maps (pixel (i, j) of level s = (i*s, j*s))
@@ -426,9 +466,8 @@ extern "C" int rk_normals_cross(const rk_sensor* s, const float* range, int32_t 
                                 float* normals, uint8_t* valid, float* surfel, void* stream) {
   int64_t total = (int64_t)batch * s->dev.H * s->dev.W;
   if (total <= 0) return RK_OK;
-  k_normals_cross<<<blocks_for(total, 256), 256, 0, S(stream)>>>(
-      s->dev, range, total, normals, valid, reinterpret_cast<float4*>(surfel),
-      (int64_t)s->dev.H * s->dev.W);
+  launch_k1(s, range, batch, normals, valid, reinterpret_cast<float4*>(surfel),
+            (int64_t)s->dev.H * s->dev.W, S(stream));
   RK_LAUNCHED("k_normals_cross");
   return RK_OK;
 }
@@ -447,8 +486,7 @@ extern "C" int rk_normals_cross_pyramid(const rk_sensor* s, const float* range, 
   }
   if (pitch < need) { rk_set_error("surfel pyramid pitch %lld < %lld", (long long)pitch, (long long)need); return RK_EGENERIC; }
   float4* pyr = reinterpret_cast<float4*>(surfel_pyr);
-  k_normals_cross<<<blocks_for(total, 256), 256, 0, S(stream)>>>(s->dev, range, total, nullptr,
-                                                                  nullptr, pyr, pitch);
+  launch_k1(s, range, batch, nullptr, nullptr, pyr, pitch, S(stream));
   int64_t off = (int64_t)H * W;
   for (int k = 0; k < n_strides; ++k) {
     const int st = strides_host[k];
