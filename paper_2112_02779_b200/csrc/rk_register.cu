@@ -28,6 +28,9 @@ using namespace rk;
 #ifndef RK_ICP_MINB
 #define RK_ICP_MINB 4
 #endif
+#ifndef RK_ICP_F32X
+#define RK_ICP_F32X 1
+#endif
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
@@ -250,6 +253,23 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   ++cnt;
 }
 
+template <int MATH, bool SMEM, bool STATS>
+__device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTables& tb, float mx,
+                                                float my, float mz, const float4* surf, int stride,
+                                                int lvl_off, int lvl_w, float inv_s, float gate2,
+                                                float inv_k, float* acc, float& cost, float& sumsq,
+                                                int& cnt);
+
+// float32 unprojection r * dir + origin and rigid move R p + t (FMA chains),
+// P = {R row-major, t} in float32
+__device__ __forceinline__ void move_f32(const float* P, float r, const float4& d, const float4& o,
+                                         float& mx, float& my, float& mz) {
+  const float px = __fmaf_rn(r, d.x, o.x), py = __fmaf_rn(r, d.y, o.y), pz = __fmaf_rn(r, d.z, o.z);
+  mx = __fmaf_rn(pz, P[2], __fmaf_rn(py, P[1], __fmaf_rn(px, P[0], P[9])));
+  my = __fmaf_rn(pz, P[5], __fmaf_rn(py, P[4], __fmaf_rn(px, P[3], P[10])));
+  mz = __fmaf_rn(pz, P[8], __fmaf_rn(py, P[7], __fmaf_rn(px, P[6], P[11])));
+}
+
 // one source point against the destination (registration.py:145-183): the
 // bit-exact float64 unprojection + FMA-chain transform, float32 projection,
 // stride-aligned pixel, then accumulate_point.
@@ -264,7 +284,17 @@ __device__ __forceinline__ void associate_point(const SensorDev& s, const RowTab
   double m[3];
   xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
              __dadd_rn(__dmul_rn(rd, dcur.y), ocur.y), __dadd_rn(__dmul_rn(rd, dcur.z), ocur.z), m);
-  const float mx = (float)m[0], my = (float)m[1], mz = (float)m[2];
+  associate_moved<MATH, SMEM, STATS>(s, tb, (float)m[0], (float)m[1], (float)m[2], surf, stride, lvl_off,
+                                     lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
+}
+
+// the association of an already transformed (float32) source point
+template <int MATH, bool SMEM, bool STATS>
+__device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTables& tb, float mx,
+                                                float my, float mz, const float4* surf, int stride,
+                                                int lvl_off, int lvl_w, float inv_s, float gate2,
+                                                float inv_k, float* acc, float& cost, float& sumsq,
+                                                int& cnt) {
   const Proj32 pr = project_f32<MATH, SMEM>(s, tb, mx, my, mz);
   if (pr.status != PROJ_OK) return;
   int ci = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f);
@@ -319,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   __shared__ double sh_tot[GROUPS][kNumAcc];
   __shared__ int sh_cnt[NW];
   __shared__ int sh_ctrl[GROUPS];
+  __shared__ float sh_pose32[GROUPS][12];
   if (gtid < 12) sh_pose[g][gtid] = A.init12[pair * 12 + gtid];
   int n_done = 0, status = RK_ICP_CONVERGED;
 #if RK_ICP_TIME_SOLVE
@@ -374,7 +405,57 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       for (int i = 0; i < 27; ++i) acc[i] = 0.0f;
       float cost = 0.0f, sumsq = 0.0f;
       int cnt = 0;
-      if (col_mode) {
+      // FAST: the source point is unprojected and moved in float32 with FMAs
+      // from the float32 ray tables and a float32 copy of the pose (a few ulp
+      // from the reference's float64-then-round point; tolerance contract,
+      // DESIGN.md §4).  CR keeps the bit-exact float64 restatement.
+      constexpr bool F32X = RK_ICP_F32X && MATH == MATH_FAST;
+      const float* P = sh_pose32[g];
+      if (F32X) {
+        if (gtid < 12) sh_pose32[g][gtid] = (float)pose[gtid];
+        group_sync<WPP>(g);
+      }
+      if (F32X && col_mode) {
+        for (int cj = gtid; cj < Ws; cj += GT) {
+          const int u = cj * stride;
+          const float4 o4 = __ldg(s.origins32 + u);
+          const float* sp = src + u;
+          const float4* dp = s.dirs32 + u;
+          float r_next = __ldg(sp);
+          float4 d_next = __ldg(dp);
+          for (int vi = 0; vi < Hs; ++vi) {
+            const float r = r_next;
+            const float4 d4 = d_next;
+            sp += row_step;
+            dp += row_step;
+            if (vi + 1 < Hs) {
+              r_next = __ldg(sp);
+              d_next = __ldg(dp);
+            }
+            if (!range_ok(r, cmin, cmax)) continue;
+            float mx, my, mz;
+            move_f32(P, r, d4, o4, mx, my, mz);
+            associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, stride, lvl_off, lvl_w, inv_s,
+                                               gate2, inv_k, acc, cost, sumsq, cnt);
+          }
+        }
+      } else if (F32X) {
+        // generic row-major walk, float32 transform
+        int off = off0, ui = ui0;
+        for (int k = gtid; k < npix; k += GT) {
+          const float r = __ldg(src + off);
+          const float4 d4 = __ldg(s.dirs32 + off);
+          const int u = ui * stride;
+          off += step_off;
+          ui += du;
+          if (ui >= Ws) { ui -= Ws; off += wrap_off; }
+          if (!range_ok(r, cmin, cmax)) continue;
+          float mx, my, mz;
+          move_f32(P, r, d4, __ldg(s.origins32 + u), mx, my, mz);
+          associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, stride, lvl_off, lvl_w, inv_s,
+                                             gate2, inv_k, acc, cost, sumsq, cnt);
+        }
+      } else if (col_mode) {
         // column-owner walk (Ws % GT == 0): each lane owns view columns
         // gtid, gtid + GT, ... and walks them down the rows with a constant
         // pointer step; the receiver origin depends on the column only
