@@ -298,7 +298,7 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
                                                 int lvl_off, int lvl_w, float inv_s, float gate2,
                                                 float inv_k, float* acc, float& cost, float& sumsq,
                                                 int& cnt) {
-  const Proj32 pr = project_f32<MATH, SMEM, RK_ICP_ELEV_ONLY != 0>(s, tb, mx, my, mz);
+  const Proj32 pr = project_f32<MATH, SMEM, RK_ICP_ELEV_ONLY ? PROJ_NO_R : PROJ_EXACT>(s, tb, mx, my, mz);
   if (pr.status != PROJ_OK) return;
   int ci = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f);
   if (ci * stride >= s.W) ci = 0;

@@ -287,6 +287,9 @@ __global__ void __launch_bounds__(kAssignThreads) k_assign_slots(GridDev g) {
   }
 }
 
+#ifndef RK_TSDF_FAST_PROJ
+#define RK_TSDF_FAST_PROJ 1
+#endif
 #ifndef RK_TSDF_EARLY_STATE
 #define RK_TSDF_EARLY_STATE 1
 #endif
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
       const float x = __fadd_rn(bx, sh_off[3 * i]);
       const float y = __fadd_rn(by, sh_off[3 * i + 1]);
       const float z = __fadd_rn(bz, sh_off[3 * i + 2]);
-      Proj32 p = project_f32<MATH, SMEM>(s, tb, x, y, z);
+      Proj32 p = project_f32<MATH, SMEM, RK_TSDF_FAST_PROJ ? PROJ_FAST_R : PROJ_EXACT>(s, tb, x, y, z);
       int col = (int)__fadd_rn(p.u, 0.5f);
       if (col == s.W) col = 0;
       const float px = __ldg(A.range + p.v * s.W + col);
