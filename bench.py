@@ -39,6 +39,10 @@ METRIC = "ICP registrations/sec (64x1024 pairs) and TSDF frames/sec @5cm, % HBM 
 ICP_BYTES_PER_PT_IT = 20      # src range 4 + dst range 4 + dst normal 12
 TSDF_BYTES_PER_VOXEL = 16     # 8 B read + 8 B write of {tsdf, weight}
 TSDF_BYTES_PER_PIXEL = 4
+TSDF_VOXEL = {"c2": 0.05, "c3": 0.10, "c5": 0.03}
+TSDF_DESC = {"c2": "C2: {n}-frame 64x1024 street sequence, TSDF 5 cm",
+             "c3": "C3: {n}-frame HDL-64 64x2048 street sequence, TSDF 10 cm",
+             "c5": "C5: {n}-frame OS-128 128x2048 street sequence, TSDF 3 cm"}
 
 
 def parse():
@@ -53,6 +57,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    # TSDF sequence shape: c2 (default; 64x1024 Ouster-like, 5 cm), c3 (HDL-64
+    # 64x2048, 10 cm), c5 (OS-128 128x2048, 3 cm) -- BASELINE.json configs
+    ap.add_argument("--tsdf-config", default="c2", choices=["c2", "c3", "c5"])
     # diagnostic only (not a bench configuration): every pair reads pool image 0's
     # destination, isolating the cost of the data-dependent surfel gather
     ap.add_argument("--diag-same-dst", action="store_true")
@@ -124,14 +131,16 @@ def make_inputs(args, rank, world, device):
     # spread concurrent CTAs over different pool images (golden-ratio stride)
     idx = (np.arange(lo, hi, dtype=np.int64) * 1237) % args.pool
     pair_idx = torch.from_numpy(idx.astype(np.int32)).to(device)
+    tintr = {"c2": intr, "c3": scenes.hdl64(), "c5": scenes.os128()}[args.tsdf_config]
     traj = scenes.street_trajectory(args.frames, seed=0)
-    frames = pipeline.render_batch(intr, street, traj)
+    frames = pipeline.render_batch(tintr, street, traj)
     poses_w = torch.from_numpy(pipeline.poses_to_rows(traj)).to(device)
     inv_w = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).to(device)
     gts = np.stack([gt.as_row12() for _, gt in pool])
     torch.cuda.synchronize()
     pair_dst = torch.zeros_like(pair_idx) if args.diag_same_dst else pair_idx
-    return dict(intr=intr, src=src, dst=dst, pair_idx=pair_idx, pair_dst=pair_dst, n_pairs=hi - lo,
+    return dict(intr=intr, tintr=tintr, src=src, dst=dst, pair_idx=pair_idx, pair_dst=pair_dst,
+                n_pairs=hi - lo,
                 frames=frames,
                 poses_w=poses_w, inv_w=inv_w, traj=traj, gts=gts)
 
@@ -141,16 +150,16 @@ class TsdfRunner:
     hash-sharded over the ranks (each integrates its own blocks for every
     frame) and rank 0 broadcasts the frames + poses over NCCL first."""
 
-    def __init__(self, intr, rank, world, dist):
+    def __init__(self, intr, rank, world, dist, voxel=0.05):
         import paper_2112_02779_b200 as rk
         from paper_2112_02779_b200 import distributed as rkd
         self.intr, self.world, self.dist = intr, world, dist
         if world > 1:
-            self.sharded = rkd.ShardedGrid(0.05, rank, world, dist, capacity=32768)
+            self.sharded = rkd.ShardedGrid(voxel, rank, world, dist, capacity=65536)
             self.grid = self.sharded.grid
         else:
             self.sharded = None
-            self.grid = rk.VoxelBlockGrid(voxel_size=0.05, capacity=32768)
+            self.grid = rk.VoxelBlockGrid(voxel_size=voxel, capacity=65536)
 
     def run(self, frames, poses_w, inv_w, updated):
         from paper_2112_02779_b200 import distributed as rkd
@@ -177,7 +186,7 @@ def run_ours(args, rank, world, dist):
     D = make_inputs(args, rank, world, device)
     intr = D["intr"]
     cfg = rk.RegistrationConfig()
-    tsdf = TsdfRunner(intr, rank, world, dist)
+    tsdf = TsdfRunner(D["tintr"], rank, world, dist, TSDF_VOXEL[args.tsdf_config])
     grid = tsdf.grid
     stream = torch.cuda.current_stream()
     pt_iters = torch.zeros(1, dtype=torch.int64, device=device)
@@ -250,7 +259,8 @@ def run_ours(args, rank, world, dist):
     icp_kernel_ms = acc["icp"] / K
     achieved = ICP_BYTES_PER_PT_IT * pt_per_launch / (icp_kernel_ms / 1e3) / 1e9
     upd_per_step = upd.item() / K
-    tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd_per_step + TSDF_BYTES_PER_PIXEL * intr.height * intr.width * args.frames
+    tin = D["tintr"]
+    tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd_per_step + TSDF_BYTES_PER_PIXEL * tin.height * tin.width * args.frames
     tsdf_achieved = tsdf_bytes / (acc["tsdf"] / K / 1e3) / 1e9
     coarse = len({s for s, _ in cfg.schedule if s > 1})
     launches = K * (1 + coarse + 1 + pipeline.LAUNCHES_CLEAR + pipeline.LAUNCHES_PER_FRAME * args.frames)
@@ -478,12 +488,13 @@ def main():
         "metric": METRIC, "value": r["reg_per_s"], "unit": "registrations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["elapsed_ms"] / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (f64 transforms/solve)", "data": "synthetic (device-rendered street scene)",
+        "dtype": "f32 (f64 solve and sensor tables)", "data": "synthetic (device-rendered street scene)",
         "config": {"workload": "C4: 65,536 independent 64x1024 Ouster-like pairs (pool of "
                                f"{args.pool} unique street pairs), 3-level ICP 4:20,2:20,1:10 + "
-                               f"C2: {args.frames}-frame 64x1024 street sequence, TSDF 5 cm",
+                               + TSDF_DESC[args.tsdf_config].format(n=args.frames),
                    "pairs": args.pairs, "pairs_per_rank": r["D"]["n_pairs"], "pool": args.pool,
-                   "frames": args.frames, "voxel_m": 0.05,
+                   "frames": args.frames, "voxel_m": TSDF_VOXEL[args.tsdf_config],
+                   "tsdf_config": args.tsdf_config,
                    "l2": "inputs > L2 (ICP pool %.1f GB)" % (args.pool * 64 * 1024 * 24 / 1e9),
                    "parallelism": f"pairs sharded over {world} rank(s)"},
         "tsdf": {"value": r["tsdf_fps"], "unit": "frames/s", "voxels_updated_per_step": r["tsdf_updated"],
