@@ -285,49 +285,62 @@ def run_ours(args, rank, world, dist):
 
 
 def run_e2e(args, rank, world, dist, D, tsdf, cfg):
-    """Same step through the public API with host buffers: pinned H2D of the
-    step's input images, D2H of poses/status and the voxel count."""
+    """Same step through the public API with host buffers: every step copies
+    its input images from pinned host memory (H2D) and reads back poses,
+    status and the voxel count (D2H).  Two device staging buffers let the
+    copy of step k+1 run on a copy stream while step k computes."""
     import torch
 
     import paper_2112_02779_b200 as rk
-    from paper_2112_02779_b200 import pipeline
     from paper_2112_02779_b200.range_image import normals_cross_batch
     src_h = D["src"].cpu().pin_memory()
     dst_h = D["dst"].cpu().pin_memory()
     frames_h = D["frames"].cpu().pin_memory()
-    # device staging buffers, refilled from pinned host memory every step
-    src = torch.empty_like(D["src"])
-    dst = torch.empty_like(D["dst"])
-    frames = torch.empty_like(D["frames"])
+    bufs = [dict(src=torch.empty_like(D["src"]), dst=torch.empty_like(D["dst"]),
+                 frames=torch.empty_like(D["frames"])) for _ in range(2)]
     upd = torch.zeros(1, dtype=torch.int64, device="cuda")
     intr = D["intr"]
+    main = torch.cuda.current_stream()
+    copy_stream = torch.cuda.Stream()
+    ev_ready = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
     h2d = src_h.numel() * 4 + dst_h.numel() * 4 + frames_h.numel() * 4
     d2h = 0
 
-    def step():
-        nonlocal d2h
-        src.copy_(src_h, non_blocking=True)
-        dst.copy_(dst_h, non_blocking=True)
-        frames.copy_(frames_h, non_blocking=True)
-        surf = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
-        res = rk.register_batch(intr, src, dst, surf, pair_src=D["pair_idx"], pair_dst=D["pair_idx"],
-                                config=cfg)
-        upd.zero_()
-        tsdf.run(frames, D["poses_w"], D["inv_w"], upd)
-        poses = res.poses.cpu()
-        status = res.status.cpu()
-        n = upd.cpu()
-        d2h = poses.numel() * 8 + status.numel() * 4 + n.numel() * 8
-        return poses
+    def issue_copy(b):
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(ev_free[b])      # no earlier step still reads buffer b
+            bufs[b]["src"].copy_(src_h, non_blocking=True)
+            bufs[b]["dst"].copy_(dst_h, non_blocking=True)
+            bufs[b]["frames"].copy_(frames_h, non_blocking=True)
+            ev_ready[b].record(copy_stream)
 
-    for _ in range(2):
-        step()
+    def run(n):
+        nonlocal d2h
+        issue_copy(0)
+        for k in range(n):
+            b = k % 2
+            if k + 1 < n:
+                issue_copy(1 - b)
+            main.wait_event(ev_ready[b])
+            src, dst, frames = bufs[b]["src"], bufs[b]["dst"], bufs[b]["frames"]
+            surf = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
+            res = rk.register_batch(intr, src, dst, surf, pair_src=D["pair_idx"],
+                                    pair_dst=D["pair_idx"], config=cfg)
+            upd.zero_()
+            tsdf.run(frames, D["poses_w"], D["inv_w"], upd)
+            ev_free[b].record(main)
+            poses = res.poses.cpu()
+            status = res.status.cpu()
+            n_upd = upd.cpu()
+            d2h = poses.numel() * 8 + status.numel() * 4 + n_upd.numel() * 8
+
+    run(2)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
+    run(args.steps)
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     if dist is not None:
@@ -337,7 +350,9 @@ def run_e2e(args, rank, world, dist, D, tsdf, cfg):
     total_pairs = args.pairs if dist is not None else D["n_pairs"]
     return dict(value=total_pairs * args.steps / el, unit="registrations/s",
                 h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
-                tsdf_frames_in_step=args.frames, seconds=el)
+                tsdf_frames_in_step=args.frames, seconds=el,
+                note="every step's inputs copied H2D inside the timed region; the copy of step "
+                     "k+1 overlaps step k (two staging buffers, copy stream)")
 
 
 # ------------------------------------------------------------------ CPU oracle
