@@ -252,15 +252,17 @@ def run_ours(args, rank, world, dist):
         pt, upd = pt_iters, updated
         total_pairs = D["n_pairs"]
     K = args.steps
+    # roofline quantities are per GPU: this rank's work over this rank's kernel time
+    pt_local, upd_local = pt_iters.item() / K, updated.item() / K
     reg_per_s = total_pairs * K / (icp_ms / 1e3)
     # the ranks share one sequence (hash-sharded blocks): strong scaling
     tsdf_fps = args.frames * K / (tsdf_ms / 1e3)
     pt_per_launch = pt.item() / K
     icp_kernel_ms = acc["icp"] / K
-    achieved = ICP_BYTES_PER_PT_IT * pt_per_launch / (icp_kernel_ms / 1e3) / 1e9
+    achieved = ICP_BYTES_PER_PT_IT * pt_local / (icp_kernel_ms / 1e3) / 1e9
     upd_per_step = upd.item() / K
     tin = D["tintr"]
-    tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd_per_step + TSDF_BYTES_PER_PIXEL * tin.height * tin.width * args.frames
+    tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd_local + TSDF_BYTES_PER_PIXEL * tin.height * tin.width * args.frames
     tsdf_achieved = tsdf_bytes / (acc["tsdf"] / K / 1e3) / 1e9
     coarse = len({s for s, _ in cfg.schedule if s > 1})
     launches = K * (1 + coarse + 1 + pipeline.LAUNCHES_CLEAR + pipeline.LAUNCHES_PER_FRAME * args.frames)
@@ -278,7 +280,8 @@ def run_ours(args, rank, world, dist):
                 "triangles": int(tri.shape[0]), "blocks": int(n_blocks)}
     return dict(reg_per_s=reg_per_s, tsdf_fps=tsdf_fps, elapsed_ms=elapsed_ms, icp_ms=icp_ms,
                 tsdf_ms=tsdf_ms, achieved=achieved, pt_per_launch=pt_per_launch,
-                icp_kernel_ms=icp_kernel_ms, normals_ms=acc["normals"] / K,
+                icp_kernel_ms=icp_kernel_ms, normals_ms=acc["normals"] / K, pt_local=pt_local,
+                upd_local=upd_local,
                 tsdf_achieved=tsdf_achieved, tsdf_updated=upd_per_step, n_blocks=n_blocks,
                 clocks=clocks.summary(), launches=launches, ok_frac=ok_frac, D=D, tsdf=tsdf, cfg=cfg,
                 mesh=mesh)
@@ -516,17 +519,17 @@ def main():
                  "blocks": r["n_blocks"],
                  "roofline": {"bound": "hbm", "achieved": r["tsdf_achieved"], "peak": peak, "unit": "GB/s",
                               "frac": r["tsdf_achieved"] / peak,
-                              "traffic": (tt * r["tsdf_updated"] if (tt := profile_traffic("k_integrate"))
+                              "traffic": (tt * r["upd_local"] if (tt := profile_traffic("k_integrate"))
                                           else None)}},
         "roofline": {"bound": "hbm", "kernel": "k_register", "achieved": r["achieved"], "peak": peak,
                      "unit": "GB/s", "frac": r["achieved"] / peak,
-                     "traffic": (tr * r["pt_per_launch"] if tr else None),
-                     "work": f"{r['pt_per_launch']:.4g} source-point-iterations x {ICP_BYTES_PER_PT_IT} B "
+                     "traffic": (tr * r["pt_local"] if tr else None),
+                     "work": f"{r['pt_local']:.4g} source-point-iterations x {ICP_BYTES_PER_PT_IT} B "
                              f"per launch, {r['icp_kernel_ms']:.2f} ms/launch", "peak_source": peak_src},
         "issue_roofline": {
-            "k_register": issue_roofline("k_register", r["pt_per_launch"], r["icp_kernel_ms"] / 1e3,
+            "k_register": issue_roofline("k_register", r["pt_local"], r["icp_kernel_ms"] / 1e3,
                                          r["clocks"].get("sm_mhz")),
-            "k_integrate": issue_roofline("k_integrate", r["tsdf_updated"],
+            "k_integrate": issue_roofline("k_integrate", r["upd_local"],
                                           r["tsdf_ms"] / args.steps / 1e3, r["clocks"].get("sm_mhz"))},
         "phase_ms": {"normals": r["normals_ms"], "register": r["icp_kernel_ms"],
                      "tsdf_sequence": r["tsdf_ms"] / args.steps},
