@@ -9,6 +9,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
+from .trace import nvtx
 from .mc_tables import TRI_TABLE
 from .sdf_volume import VoxelBlockGrid
 
@@ -68,6 +69,7 @@ def extract_mesh_device(grid: VoxelBlockGrid, min_weight: float = 1.0):
     return v, t, n
 
 
+@nvtx("extract_mesh")
 def extract_mesh(grid: VoxelBlockGrid, min_weight: float = 1.0) -> TriangleMesh:
     """Marching Cubes over every cell whose 8 corners have weight >= min_weight
     (mesh_extract.py:85-178)."""

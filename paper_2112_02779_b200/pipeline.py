@@ -14,6 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as nat
+from .trace import nvtx
 from . import lidar_model as lm
 from .distributed import all_gather_varsize, shard  # noqa: F401  (re-exported)
 from .sdf_volume import VoxelBlockGrid
@@ -58,6 +59,7 @@ def render_batch(intr: lm.LidarIntrinsics, scene, poses):
     return out
 
 
+@nvtx("integrate_sequence")
 def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, poses_w,
                        inv_w=None, clip_min: float = 0.0, clip_max: float = np.inf,
                        radius: float | None = None, updated=None, graph: bool = False):

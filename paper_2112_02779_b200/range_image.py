@@ -15,6 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
+from .trace import nvtx
 from . import lidar_model as lm
 from .errors import InvalidIntrinsics
 from .lidar_model import LidarIntrinsics
@@ -267,6 +268,7 @@ def points_at_stride(img: RangeImage, stride: int, clip_min: float = 0.0,
     return _ret(img, _points_from_indices(img, idx, cnt))
 
 
+@nvtx("compute_normal_map")
 def compute_normal_map(img: RangeImage, method: str = "cross", radius: int = 2,
                        discontinuity_abs: float = DISCONTINUITY_ABS,
                        discontinuity_rel: float = DISCONTINUITY_REL) -> NormalImage:
@@ -323,6 +325,7 @@ class SurfelPyramid:
     offsets: dict
 
 
+@nvtx("normals_cross_batch")
 def normals_cross_batch(intr: LidarIntrinsics, ranges, strides=None):
     """K1 over a (B, H, W) device batch -> (B, H, W, 4) surfel maps (batch
     API), or with ``strides`` a SurfelPyramid whose coarse levels the
@@ -358,6 +361,7 @@ class ProjectionStats:
     degenerate: int = 0
 
 
+@nvtx("from_point_cloud")
 def from_point_cloud(points, intr: LidarIntrinsics, max_iters: int = 3, tol: float = 1e-4):
     """Project a cloud into a fresh image, nearest range wins pixel collisions
     (range_image.py:170-194): the float64 projection (rk_project_f64) then a

@@ -17,6 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
+from .trace import nvtx
 from . import lidar_model as lm
 from .errors import DegenerateGeometry, EmptyInput, MissingNormals
 from .range_image import (NormalImage, RangeImage, SurfelPyramid, compute_normal_map,
@@ -248,6 +249,7 @@ class BatchResult:
         return RigidTransform(p[:9].reshape(3, 3), p[9:])
 
 
+@nvtx("register_batch")
 def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels=None,
                    pair_src=None, pair_dst=None, inits=None,
                    config: RegistrationConfig = RegistrationConfig(), with_stats: bool = False,
@@ -298,6 +300,7 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     return BatchResult(poses, status, iters, stats)
 
 
+@nvtx("register")
 def register(src_img: RangeImage, dst_img: RangeImage, init: RigidTransform | None = None,
              config: RegistrationConfig = RegistrationConfig(),
              dst_normals: NormalImage | None = None) -> RegistrationResult:

@@ -18,6 +18,7 @@ from itertools import product
 import numpy as np
 
 from . import _native as nat
+from .trace import nvtx
 from . import lidar_model as lm
 from .errors import InvalidPose
 from .range_image import RangeImage
@@ -372,6 +373,7 @@ def _integrate_touched(grid, img, pose, clip_min, clip_max, sync=True):
     return int(updated.item()) if sync else updated
 
 
+@nvtx("integrate_cloud_frame")
 def integrate_cloud_frame(grid: VoxelBlockGrid, img: RangeImage, pose_frame_to_world: RigidTransform,
                           activation_radius: float | None = None, clip_min: float = 0.0,
                           clip_max: float = np.inf, threads: int | None = None) -> int:

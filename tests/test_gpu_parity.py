@@ -689,3 +689,17 @@ def test_register_single_plane_is_degenerate(rk, sensors, osensors):
     t = torch.from_numpy(img).cuda()[None].repeat(2, 1, 1)
     res = rk.register_batch(intr, t, t)
     assert res.status.tolist() == [2, 2]
+
+
+def test_nvtx_tracing_is_transparent(rk, sensors, golden_icp):
+    """RK_NVTX-style tracing wraps the public calls without changing results."""
+    from paper_2112_02779_b200 import trace
+    intr = sensors["synth"]
+    src, dst = rk.RangeImage(golden_icp["synth/src"], intr), rk.RangeImage(golden_icp["synth/dst"], intr)
+    a = rk.register(src, dst)
+    trace.enable(True)
+    try:
+        b = rk.register(src, dst)
+    finally:
+        trace.enable(False)
+    assert np.array_equal(a.pose.matrix(), b.pose.matrix())
