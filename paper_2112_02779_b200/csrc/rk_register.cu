@@ -31,6 +31,9 @@ using namespace rk;
 #ifndef RK_ICP_F32X
 #define RK_ICP_F32X 1
 #endif
+#ifndef RK_ICP_FUSED
+#define RK_ICP_FUSED 1
+#endif
 #ifndef RK_ICP_ELEV_ONLY
 #define RK_ICP_ELEV_ONLY 1
 #endif
@@ -212,26 +215,44 @@ __device__ __forceinline__ double warp_sum(double v) {
 // association tail + point-to-plane terms of one correspondence
 // (registration.py:168-183, 339-352): gate on the stored target, residual,
 // Jacobian, pseudo-Huber IRLS weight, 27 float32 accumulations.
-template <bool STATS>
+// FUSED (K3 in MATH_FAST): the same expressions as FMA chains (~1 ulp, the
+// tolerance class of the float32 move); otherwise the reference's separate
+// roundings, so MATH_CR associates exactly like the oracle.
+template <bool STATS, bool FUSED = false>
 __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, const float4& n,
                                                  const float4& d, const float4& o, float gate2,
                                                  float inv_k, float* acc, float& cost, float& sumsq,
                                                  int& cnt) {
   if (!(n.w > 0.0f)) return;  // stored range > 0 and normal valid
-  const float qx = __fadd_rn(__fmul_rn(n.w, d.x), o.x);
-  const float qy = __fadd_rn(__fmul_rn(n.w, d.y), o.y);
-  const float qz = __fadd_rn(__fmul_rn(n.w, d.z), o.z);
-  const float dx = __fsub_rn(mx, qx), dy = __fsub_rn(my, qy), dz = __fsub_rn(mz, qz);
-  const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-  if (!(d2 <= gate2)) return;
-  // ---- residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352).
-  // Only the reduced sums matter here (pose tolerance 1e-5), so the
-  // weight uses the fast reciprocal square root.
-  const float res = __fadd_rn(__fadd_rn(__fmul_rn(n.x, dx), __fmul_rn(n.y, dy)), __fmul_rn(n.z, dz));
+  float dx, dy, dz, d2, res;
   float J[6];
-  J[0] = __fsub_rn(__fmul_rn(my, n.z), __fmul_rn(mz, n.y));
-  J[1] = __fsub_rn(__fmul_rn(mz, n.x), __fmul_rn(mx, n.z));
-  J[2] = __fsub_rn(__fmul_rn(mx, n.y), __fmul_rn(my, n.x));
+  if (FUSED) {
+    dx = __fsub_rn(mx, __fmaf_rn(n.w, d.x, o.x));
+    dy = __fsub_rn(my, __fmaf_rn(n.w, d.y, o.y));
+    dz = __fsub_rn(mz, __fmaf_rn(n.w, d.z, o.z));
+    d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    if (!(d2 <= gate2)) return;
+    res = __fmaf_rn(n.z, dz, __fmaf_rn(n.y, dy, __fmul_rn(n.x, dx)));
+    J[0] = __fmaf_rn(my, n.z, -__fmul_rn(mz, n.y));
+    J[1] = __fmaf_rn(mz, n.x, -__fmul_rn(mx, n.z));
+    J[2] = __fmaf_rn(mx, n.y, -__fmul_rn(my, n.x));
+  } else {
+    const float qx = __fadd_rn(__fmul_rn(n.w, d.x), o.x);
+    const float qy = __fadd_rn(__fmul_rn(n.w, d.y), o.y);
+    const float qz = __fadd_rn(__fmul_rn(n.w, d.z), o.z);
+    dx = __fsub_rn(mx, qx);
+    dy = __fsub_rn(my, qy);
+    dz = __fsub_rn(mz, qz);
+    d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+    if (!(d2 <= gate2)) return;
+    // ---- residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352).
+    // Only the reduced sums matter here (pose tolerance 1e-5), so the
+    // weight uses the fast reciprocal square root.
+    res = __fadd_rn(__fadd_rn(__fmul_rn(n.x, dx), __fmul_rn(n.y, dy)), __fmul_rn(n.z, dz));
+    J[0] = __fsub_rn(__fmul_rn(my, n.z), __fmul_rn(mz, n.y));
+    J[1] = __fsub_rn(__fmul_rn(mz, n.x), __fmul_rn(mx, n.z));
+    J[2] = __fsub_rn(__fmul_rn(mx, n.y), __fmul_rn(my, n.x));
+  }
   J[3] = n.x;
   J[4] = n.y;
   J[5] = n.z;
@@ -310,7 +331,8 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
   const float4 n = __ldg(surf + (lvl_w ? lvl_off + ri * lvl_w + ci : flat));
   const float4 d = __ldg(s.dirs32 + flat);
   const float4 o = __ldg(s.origins32 + col);
-  accumulate_point<STATS>(mx, my, mz, n, d, o, gate2, inv_k, acc, cost, sumsq, cnt);
+  accumulate_point<STATS, RK_ICP_FUSED && MATH == MATH_FAST>(mx, my, mz, n, d, o, gate2, inv_k, acc,
+                                                            cost, sumsq, cnt);
 }
 
 template <int WPP>
