@@ -97,6 +97,7 @@ extern "C" int rk_sensor_create(const rk_sensor_desc* d, rk_sensor** out) {
   v.inv_scale = (double)(K - 1) / (d->inv_phi_max - d->inv_phi_min);
   v.inv_lo32 = (float)v.inv_lo;
   v.inv_scale32 = (float)v.inv_scale;
+  v.inv_off32 = (float)(0.5 - v.inv_lo * v.inv_scale);
   v.fov_lo = d->fov_lo; v.fov_hi = d->fov_hi;
   v.fov_lo32 = (float)d->fov_lo; v.fov_hi32 = (float)d->fov_hi;
   v.cpr = (double)W / kTwoPi;
