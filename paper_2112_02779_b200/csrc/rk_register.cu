@@ -218,18 +218,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 // FUSED (K3 in MATH_FAST): the same expressions as FMA chains (~1 ulp, the
 // tolerance class of the float32 move); otherwise the reference's separate
 // roundings, so MATH_CR associates exactly like the oracle.
+// q: the association target {x, y, z} (registration.py:168-176), from the
+// surfel pyramid record or formed from the ray tables by the caller.
 template <bool STATS, bool FUSED = false>
 __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, const float4& n,
-                                                 const float4& d, const float4& o, float gate2,
-                                                 float inv_k, float* acc, float& cost, float& sumsq,
-                                                 int& cnt) {
+                                                 const float4& q, float gate2, float inv_k,
+                                                 float* acc, float& cost, float& sumsq, int& cnt) {
   if (!(n.w > 0.0f)) return;  // stored range > 0 and normal valid
   float dx, dy, dz, d2, res;
   float J[6];
   if (FUSED) {
-    dx = __fsub_rn(mx, __fmaf_rn(n.w, d.x, o.x));
-    dy = __fsub_rn(my, __fmaf_rn(n.w, d.y, o.y));
-    dz = __fsub_rn(mz, __fmaf_rn(n.w, d.z, o.z));
+    dx = __fsub_rn(mx, q.x);
+    dy = __fsub_rn(my, q.y);
+    dz = __fsub_rn(mz, q.z);
     d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
     if (!(d2 <= gate2)) return;
     res = __fmaf_rn(n.z, dz, __fmaf_rn(n.y, dy, __fmul_rn(n.x, dx)));
@@ -237,12 +238,9 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
     J[1] = __fmaf_rn(mz, n.x, -__fmul_rn(mx, n.z));
     J[2] = __fmaf_rn(mx, n.y, -__fmul_rn(my, n.x));
   } else {
-    const float qx = __fadd_rn(__fmul_rn(n.w, d.x), o.x);
-    const float qy = __fadd_rn(__fmul_rn(n.w, d.y), o.y);
-    const float qz = __fadd_rn(__fmul_rn(n.w, d.z), o.z);
-    dx = __fsub_rn(mx, qx);
-    dy = __fsub_rn(my, qy);
-    dz = __fsub_rn(mz, qz);
+    dx = __fsub_rn(mx, q.x);
+    dy = __fsub_rn(my, q.y);
+    dz = __fsub_rn(mz, q.z);
     d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
     if (!(d2 <= gate2)) return;
     // ---- residual, Jacobian, pseudo-Huber IRLS weight (registration.py:339-352).
@@ -260,12 +258,12 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   const float s1 = __fmaf_rn(e, e, 1.0f);
   const float w = rsqrtf(s1);
   const float rw = -res * w;
-  int q = 0;
+  int h = 0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const float jw = J[i] * w;
 #pragma unroll
-    for (int j = i; j < 6; ++j) { acc[q] = __fmaf_rn(jw, J[j], acc[q]); ++q; }
+    for (int j = i; j < 6; ++j) { acc[h] = __fmaf_rn(jw, J[j], acc[h]); ++h; }
   }
 #pragma unroll
   for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
@@ -279,10 +277,10 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
 
 template <int MATH, bool SMEM, bool STATS>
 __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTables& tb, float mx,
-                                                float my, float mz, const float4* surf, int stride,
-                                                int lvl_off, int lvl_w, float inv_s, float gate2,
-                                                float inv_k, float* acc, float& cost, float& sumsq,
-                                                int& cnt);
+                                                float my, float mz, const float4* surf, bool lvl_rec,
+                                                int stride, int lvl_off, int lvl_w, float inv_s,
+                                                float gate2, float inv_k, float* acc, float& cost,
+                                                float& sumsq, int& cnt);
 
 // float32 unprojection r * dir + origin and rigid move R p + t (FMA chains),
 // P = {R row-major, t} in float32
@@ -300,25 +298,25 @@ __device__ __forceinline__ void move_f32(const float* P, float r, const float4& 
 template <int MATH, bool SMEM, bool STATS>
 __device__ __forceinline__ void associate_point(const SensorDev& s, const RowTables& tb,
                                                 const double* pose, float r, const double3& dcur,
-                                                const double3& ocur, const float4* surf, int stride,
-                                                int lvl_off, int lvl_w, float inv_s, float gate2,
-                                                float inv_k, float* acc, float& cost, float& sumsq,
-                                                int& cnt) {
+                                                const double3& ocur, const float4* surf, bool lvl_rec,
+                                                int stride, int lvl_off, int lvl_w, float inv_s,
+                                                float gate2, float inv_k, float* acc, float& cost,
+                                                float& sumsq, int& cnt) {
   const double rd = (double)r;
   double m[3];
   xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
              __dadd_rn(__dmul_rn(rd, dcur.y), ocur.y), __dadd_rn(__dmul_rn(rd, dcur.z), ocur.z), m);
-  associate_moved<MATH, SMEM, STATS>(s, tb, (float)m[0], (float)m[1], (float)m[2], surf, stride, lvl_off,
+  associate_moved<MATH, SMEM, STATS>(s, tb, (float)m[0], (float)m[1], (float)m[2], surf, lvl_rec, stride, lvl_off,
                                      lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
 }
 
 // the association of an already transformed (float32) source point
 template <int MATH, bool SMEM, bool STATS>
 __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTables& tb, float mx,
-                                                float my, float mz, const float4* surf, int stride,
-                                                int lvl_off, int lvl_w, float inv_s, float gate2,
-                                                float inv_k, float* acc, float& cost, float& sumsq,
-                                                int& cnt) {
+                                                float my, float mz, const float4* surf, bool lvl_rec,
+                                                int stride, int lvl_off, int lvl_w, float inv_s,
+                                                float gate2, float inv_k, float* acc, float& cost,
+                                                float& sumsq, int& cnt) {
   const Proj32 pr = project_f32<MATH, SMEM, RK_ICP_ELEV_ONLY ? PROJ_NO_R : PROJ_EXACT>(s, tb, mx, my, mz);
   if (pr.status != PROJ_OK) return;
   int ci = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f);
@@ -327,12 +325,24 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
   const int col = ci * stride, row = ri * stride;
   if (row >= s.H) return;  // dropped, not clamped (registration.py:157-159)
   const int flat = row * s.W + col;
-  // the level's compact decimated map when the caller built a pyramid
-  const float4 n = __ldg(surf + (lvl_w ? lvl_off + ri * lvl_w + ci : flat));
-  const float4 d = __ldg(s.dirs32 + flat);
-  const float4 o = __ldg(s.origins32 + col);
-  accumulate_point<STATS, RK_ICP_FUSED && MATH == MATH_FAST>(mx, my, mz, n, d, o, gate2, inv_k, acc,
-                                                            cost, sumsq, cnt);
+  constexpr bool FUSED = RK_ICP_FUSED && MATH == MATH_FAST;
+  float4 n, q;
+  if (lvl_rec) {
+    // surfel pyramid: 32-byte {n, range} + {target} records; the level's
+    // compact decimated map (lvl_w > 0) or the full map (level stride 1)
+    const int idx = lvl_w ? lvl_off + ri * lvl_w + ci : flat;
+    n = __ldg(surf + 2 * idx);
+    q = __ldg(surf + 2 * idx + 1);
+  } else {
+    n = __ldg(surf + flat);
+    const float4 d = __ldg(s.dirs32 + flat);
+    const float4 o = __ldg(s.origins32 + col);
+    // the reference's target (registration.py:168-176), exactly as the
+    // pyramid records hold it, so both layouts associate identically
+    q = make_float4(__fadd_rn(__fmul_rn(n.w, d.x), o.x), __fadd_rn(__fmul_rn(n.w, d.y), o.y),
+                    __fadd_rn(__fmul_rn(n.w, d.z), o.z), 0.f);
+  }
+  accumulate_point<STATS, FUSED>(mx, my, mz, n, q, gate2, inv_k, acc, cost, sumsq, cnt);
 }
 
 template <int WPP>
@@ -366,7 +376,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   const int H = s.H, W = s.W;
   const size_t HW = (size_t)H * W;
   const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
-  const long long surf_pitch = A.cfg.surfel_pitch ? A.cfg.surfel_pitch : (long long)HW;
+  // a surfel pyramid (surfel_pitch != 0) holds 32-byte records {n, range},
+  // {target}; a plain surfel map 16-byte {n, range}
+  const bool rec = A.cfg.surfel_pitch != 0;
+  const long long surf_pitch = rec ? 2 * A.cfg.surfel_pitch : (long long)HW;
   const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * surf_pitch;
 
   __shared__ double sh_pose[GROUPS][12];
@@ -460,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
             if (!range_ok(r, cmin, cmax)) continue;
             float mx, my, mz;
             move_f32(P, r, d4, o4, mx, my, mz);
-            associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, stride, lvl_off, lvl_w, inv_s,
+            associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, stride, lvl_off, lvl_w, inv_s,
                                                gate2, inv_k, acc, cost, sumsq, cnt);
           }
         }
@@ -477,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           if (!range_ok(r, cmin, cmax)) continue;
           float mx, my, mz;
           move_f32(P, r, d4, __ldg(s.origins32 + u), mx, my, mz);
-          associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, stride, lvl_off, lvl_w, inv_s,
+          associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, stride, lvl_off, lvl_w, inv_s,
                                              gate2, inv_k, acc, cost, sumsq, cnt);
         }
       } else if (col_mode) {
@@ -502,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
               d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
             }
             if (!range_ok(r, cmin, cmax)) continue;
-            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, lvl_off,
+            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
                                                lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
           }
         }
@@ -531,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           if (!range_ok(r, cmin, cmax)) continue;
           const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
                                             __ldg(s.origins + 3 * u + 2));
-          associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, stride, lvl_off,
+          associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
                                              lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
         }
       }

@@ -367,7 +367,7 @@ extern "C" int rk_unproject_image(const rk_sensor* s, const float* range, int32_
 constexpr int K1_TW = 128, K1_TH = 8, K1_THREADS = 256;
 __global__ void __launch_bounds__(K1_THREADS) k_normals_cross(
     SensorDev s, const float* __restrict__ range, int batch, float* normals, uint8_t* valid,
-    float4* surfel, int64_t surfel_pitch) {
+    float4* surfel, int64_t surfel_pitch, int targets) {
   constexpr int PW = K1_TW + 1, PH = K1_TH + 1;
   __shared__ double sp[3][PH * PW];
   __shared__ float sr[PH * PW];
@@ -436,16 +436,30 @@ __global__ void __launch_bounds__(K1_THREADS) k_normals_cross(
       normals[3 * i + 2] = n2;
     }
     if (valid) valid[i] = ok ? 1 : 0;
-    if (surfel) surfel[img * surfel_pitch + p] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+    if (surfel) {
+      if (targets) {
+        // pyramid layout: {n, range} then the association target
+        // r * dir32 + origin32 with the reference's separate roundings
+        // (registration.py:168-176), so the registration gathers one
+        // 32-byte record instead of also reading the ray tables
+        const float4 d = __ldg(s.dirs32 + p), o = __ldg(s.origins32 + u);
+        float4* rec = surfel + 2 * (img * surfel_pitch + p);
+        rec[0] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+        rec[1] = make_float4(__fadd_rn(__fmul_rn(r0, d.x), o.x), __fadd_rn(__fmul_rn(r0, d.y), o.y),
+                             __fadd_rn(__fmul_rn(r0, d.z), o.z), 0.f);
+      } else {
+        surfel[img * surfel_pitch + p] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+      }
+    }
   }
 }
 
 static void launch_k1(const rk_sensor* s, const float* range, int32_t batch, float* normals,
-                      uint8_t* valid, float4* surfel, int64_t pitch, cudaStream_t st) {
+                      uint8_t* valid, float4* surfel, int64_t pitch, cudaStream_t st, int targets = 0) {
   const int W = s->dev.W, H = s->dev.H;
   const unsigned tiles = (unsigned)(((W + K1_TW - 1) / K1_TW) * ((H + K1_TH - 1) / K1_TH));
   k_normals_cross<<<tiles * (unsigned)batch, K1_THREADS, 0, st>>>(s->dev, range, batch, normals,
-                                                                  valid, surfel, pitch);
+                                                                  valid, surfel, pitch, targets);
 }
 
 // decimated copies of the full surfel maps (pixel (i, j) of level s = (i*s, j*s))
@@ -458,8 +472,10 @@ __global__ void k_surfel_decimate(int H, int W, int batch, float4* pyr, int64_t 
     const int64_t img = k / per;
     const int q = (int)(k - img * per);
     const int i = q / Ws, j = q - i * Ws;
-    float4* base = pyr + img * pitch;
-    base[off + q] = base[(int64_t)i * stride * W + (int64_t)j * stride];
+    float4* base = pyr + 2 * img * pitch;  // 2 float4 records (see k_normals_cross)
+    const int64_t from = (int64_t)i * stride * W + (int64_t)j * stride;
+    base[2 * (off + q)] = base[2 * from];
+    base[2 * (off + q) + 1] = base[2 * from + 1];
   }
 }
 
@@ -487,7 +503,7 @@ extern "C" int rk_normals_cross_pyramid(const rk_sensor* s, const float* range, 
   }
   if (pitch < need) { rk_set_error("surfel pyramid pitch %lld < %lld", (long long)pitch, (long long)need); return RK_EGENERIC; }
   float4* pyr = reinterpret_cast<float4*>(surfel_pyr);
-  launch_k1(s, range, batch, nullptr, nullptr, pyr, pitch, S(stream));
+  launch_k1(s, range, batch, nullptr, nullptr, pyr, pitch, S(stream), 1);
   int64_t off = (int64_t)H * W;
   for (int k = 0; k < n_strides; ++k) {
     const int st = strides_host[k];

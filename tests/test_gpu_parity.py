@@ -282,7 +282,15 @@ def test_register_batch_surfel_pyramid_bitidentical(rk, pair, sensors, golden_ic
     flat = normals_cross_batch(intr, dst)
     pyr = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
     assert isinstance(pyr, SurfelPyramid) and set(pyr.offsets) == {1, 2, 3, 4}
-    assert torch.equal(pyr.data[:, :intr.height * intr.width].reshape(flat.shape), flat)
+    HW = intr.height * intr.width
+    assert torch.equal(pyr.data[:, :HW, :4].reshape(flat.shape), flat)
+    # the record's target is the reference's float32 r * dir32 + origin32 (registration.py:168-176)
+    d32 = np.stack(intr.ray_tables_flat_f32[0], -1)
+    o32 = np.stack(intr.ray_tables_flat_f32[1], -1)
+    r = g[f"{pair}/dst"].reshape(-1).astype(np.float32)
+    tgt = r[:, None] * d32 + o32[np.arange(HW) % intr.width]
+    got = pyr.data[0, :HW, 4:7].cpu().numpy()
+    assert np.array_equal(got[r > 0], tgt[r > 0])
     a = rk.register_batch(intr, src, dst, flat, config=cfg, with_stats=True)
     b = rk.register_batch(intr, src, dst, pyr, config=cfg, with_stats=True)
     assert torch.equal(a.poses, b.poses) and torch.equal(a.iterations, b.iterations)
