@@ -75,6 +75,14 @@ __device__ __forceinline__ float2 sample(const GridView& g, const int* nb, int x
   return g.vox[(size_t)slot * kVox + (lx * kEdge + ly) * kEdge + lz];
 }
 
+// a hash-sharded grid (rk_grid_set_shard) meshes only the blocks it owns;
+// blocks it holds as halo copies of other ranks' blocks only feed the samples
+__device__ __forceinline__ bool foreign_block(const GridView& g, int slot) {
+  if (g.shard_world <= 1) return false;
+  const int4 k = g.block_keys[slot];
+  return rk_block_owner_of(k.x, k.y, k.z, g.shard_world) != g.shard_rank;
+}
+
 __device__ __forceinline__ void load_neighbours(const GridView& g, int slot, int* nb) {
   if (threadIdx.x < 27) {
     int4 k = g.block_keys[slot];
@@ -101,6 +109,7 @@ __device__ __forceinline__ int cell_case(const GridView& g, const int* nb, int l
 
 __global__ void k_mc_count(GridView g, const int8_t* __restrict__ table, float min_w,
                            unsigned long long* counters) {
+  if (foreign_block(g, blockIdx.x)) return;  // uniform per CTA
   __shared__ int nb[27];
   __shared__ int8_t tab[256 * 16];
   for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) tab[i] = table[i];
@@ -203,6 +212,7 @@ __device__ int vertex_of(const GridView& g, const Mesh& m, const int* nb, int4 b
 
 __global__ void k_mc_vertices(GridView g, const int8_t* __restrict__ table, float min_w, double voxel,
                               Mesh m) {
+  if (foreign_block(g, blockIdx.x)) return;
   __shared__ int nb[27];
   __shared__ int8_t tab[256 * 16];
   for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) tab[i] = table[i];
@@ -236,6 +246,7 @@ __device__ __forceinline__ int find_vertex(const Mesh& m, unsigned long long key
 }
 
 __global__ void k_mc_triangles(GridView g, const int8_t* __restrict__ table, float min_w, Mesh m) {
+  if (foreign_block(g, blockIdx.x)) return;
   __shared__ int nb[27];
   __shared__ int8_t tab[256 * 16];
   for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) tab[i] = table[i];

@@ -82,16 +82,6 @@ struct GridDev {
   int shard_rank, shard_world;  // multi-GPU: this grid keeps owner(key) == rank
 };
 
-// owner of a block in a hash-sharded multi-GPU grid
-__host__ __device__ __forceinline__ unsigned long long owner_mix(unsigned long long k) {
-  k ^= k >> 31;
-  k *= 0x7fb5d329728ea185ull;
-  k ^= k >> 27;
-  k *= 0x81dadef4bc2dd44dull;
-  k ^= k >> 33;
-  return k;
-}
-
 // find or insert; returns hash position or -1 when the probe budget is spent
 __device__ long long hash_acquire(const GridDev& g, unsigned long long key, bool& inserted) {
   unsigned long long h = mix64(key) & g.hash_mask;
@@ -123,7 +113,7 @@ __device__ long long hash_find(const GridDev& g, unsigned long long key) {
 // one touched key: insert, dedupe per frame, remember fresh keys
 __device__ __forceinline__ void touch_key(const GridDev& g, int frame, long long x, long long y, long long z) {
   unsigned long long key = pack_key(x, y, z);
-  if (g.shard_world > 1 && (int)(owner_mix(key) % (unsigned long long)g.shard_world) != g.shard_rank)
+  if (g.shard_world > 1 && (int)(rk_owner_mix(key) % (unsigned long long)g.shard_world) != g.shard_rank)
     return;  // another GPU owns this block
   bool inserted;
   long long h = hash_acquire(g, key, inserted);
@@ -991,6 +981,8 @@ int rk_grid_view_(rk_grid* g, GridView* v) {
   v->h_slot = g->d.h_slot;
   v->hash_mask = g->d.hash_mask;
   v->n_blocks = c.n_blocks;
+  v->shard_rank = g->d.shard_rank;
+  v->shard_world = g->d.shard_world;
   return RK_OK;
 }
 
@@ -1030,7 +1022,7 @@ extern "C" int rk_grid_clear(rk_grid* g, void* stream) {
 }
 
 // multi-GPU hash sharding: from now on this grid only allocates blocks with
-// owner_mix(packed key) % world == rank
+// rk_owner_mix(packed key) % world == rank
 extern "C" int rk_grid_set_shard(rk_grid* g, int32_t rank, int32_t world) {
   if (world < 1 || rank < 0 || rank >= world) {
     rk_set_error("bad shard rank %d / world %d", rank, world);
@@ -1045,7 +1037,7 @@ extern "C" int rk_grid_set_shard(rk_grid* g, int32_t rank, int32_t world) {
 extern "C" int rk_block_owner(const int32_t* keys_host, int64_t n, int32_t world, int32_t* owner_host) {
   for (int64_t i = 0; i < n; ++i) {
     unsigned long long key = pack_key(keys_host[3 * i], keys_host[3 * i + 1], keys_host[3 * i + 2]);
-    owner_host[i] = (int32_t)(owner_mix(key) % (unsigned long long)world);
+    owner_host[i] = (int32_t)(rk_owner_mix(key) % (unsigned long long)world);
   }
   return RK_OK;
 }

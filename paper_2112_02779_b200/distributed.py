@@ -7,7 +7,10 @@ shard:
   integrates only blocks with ``owner(key) == r`` (``rk_grid_set_shard``).
   Per frame the range image + pose are broadcast once; the frame's touched
   count / largest key are reduced so every rank reproduces the reference's
-  sorted-chunk arithmetic; before meshing every rank's blocks are gathered.
+  sorted-chunk arithmetic.  Meshing: each rank receives the halo blocks it
+  needs (26-neighbours owned elsewhere) in one all-to-all, runs marching
+  cubes on its own blocks, and the partial meshes are gathered and merged by
+  exact vertex position (the reference's own dedup rule).
 
 The communication helpers take plain tensors so they run under the ``gloo``
 backend on CPU as well (tests/test_distributed.py); ``ShardedGrid`` adds the
@@ -151,6 +154,47 @@ class ShardedGrid:
         g.blocks._bump()
         return updated
 
+    def extract_mesh(self, min_weight: float = 1.0):
+        """Distributed marching cubes: one all-to-all of halo blocks, MC on the
+        owned blocks, one gather of the partial meshes, exact-position merge.
+        Returns a host TriangleMesh on every rank."""
+        import torch
+
+        from .mesh_extract import TriangleMesh
+        d, world, rank = self.dist, self.world, self.rank
+        keys, vox = self.grid.export_blocks(device=True)
+        if world == 1:
+            V, T, N = merge_meshes([mesh_from_shard(self.grid, 0, 1, min_weight=min_weight)])
+            return TriangleMesh(V, T, N)
+        all_keys = all_gather_varsize(keys, d)
+        n = torch.tensor([keys.shape[0]], dtype=torch.int64, device=keys.device)
+        counts = [torch.zeros_like(n) for _ in range(world)]
+        d.all_gather(counts, n)
+        counts = [int(c.item()) for c in counts]
+        host = nat.to_host(all_keys)
+        bounds = np.cumsum([0] + counts)
+        plan = halo_plan([host[bounds[q]:bounds[q + 1]] for q in range(world)])
+        send_idx = np.concatenate([plan[rank][s_] for s_ in range(world)]).astype(np.int64)
+        in_split = [int(plan[rank][s_].size) for s_ in range(world)]
+        out_split = [int(plan[q][rank].size) for q in range(world)]
+        sel = torch.from_numpy(send_idx).to(keys.device)
+        k_send = keys[sel].contiguous()
+        v_send = vox[sel].reshape(-1, 8192).contiguous()
+        k_recv = torch.empty((sum(out_split), 3), dtype=keys.dtype, device=keys.device)
+        v_recv = torch.empty((sum(out_split), 8192), dtype=vox.dtype, device=vox.device)
+        d.all_to_all_single(k_recv, k_send, out_split, in_split)
+        d.all_to_all_single(v_recv, v_send, out_split, in_split)
+        V, T, N = mesh_from_shard(self.grid, rank, world, k_recv, v_recv, min_weight)
+        nv = torch.tensor([V.shape[0]], dtype=torch.int64, device=V.device)
+        nvs = [torch.zeros_like(nv) for _ in range(world)]
+        d.all_gather(nvs, nv)
+        base = sum(int(c.item()) for c in nvs[:rank])
+        Vg = all_gather_varsize(V, d)
+        Ng = all_gather_varsize(N, d)
+        Tg = all_gather_varsize(T.to(torch.int64) + base, d)
+        Vm, Tm, Nm = merge_meshes([(Vg, Tg, Ng)])
+        return TriangleMesh(Vm, Tm, Nm)
+
     def gather_blocks(self):
         """All ranks' (keys (n,3) int32, voxels (n,4096,2) float32), device, rank order."""
         g = self.grid
@@ -175,3 +219,71 @@ class ShardedGrid:
                      nat.ptr(vox.contiguous()), nat.stream_ptr())
             out.blocks._bump()
         return out
+
+
+# ---------------------------------------------------------------- sharded meshing
+
+_NEIGH = np.array([(dx, dy, dz) for dx in (-1, 0, 1) for dy in (-1, 0, 1) for dz in (-1, 0, 1)
+                   if (dx, dy, dz) != (0, 0, 0)], dtype=np.int64)
+
+
+def _codes(keys) -> np.ndarray:
+    k = np.asarray(keys, dtype=np.int64).reshape(-1, 3) + (1 << 17)
+    return (k[:, 0] << 36) | (k[:, 1] << 18) | k[:, 2]   # sdf_volume.py:64-71 packing
+
+
+def halo_plan(keys_by_rank):
+    """send[r][s]: indices into rank r's block list of the blocks rank s needs
+    as halo (26-neighbours of s's blocks that r owns; marching cubes reads a
+    19^3 window, mesh_extract.py:58-82).  Identical on every rank."""
+    world = len(keys_by_rank)
+    codes = [_codes(k) for k in keys_by_rank]
+    send = [[np.zeros(0, np.int64) for _ in range(world)] for _ in range(world)]
+    for s_ in range(world):
+        k = np.asarray(keys_by_rank[s_], dtype=np.int64).reshape(-1, 3)
+        if k.shape[0] == 0:
+            continue
+        need = np.unique(_codes((k[:, None, :] + _NEIGH[None]).reshape(-1, 3)))
+        for r in range(world):
+            if r != s_ and codes[r].size:
+                send[r][s_] = np.flatnonzero(np.isin(codes[r], need))
+    return send
+
+
+def mesh_from_shard(grid, rank: int, world: int, halo_keys=None, halo_vox=None,
+                    min_weight: float = 1.0):
+    """Marching cubes over the blocks this rank owns, with the halo blocks of
+    other ranks as read-only neighbours: (V, T, N) CUDA tensors."""
+    from .mesh_extract import extract_mesh_device
+    from .sdf_volume import VoxelBlockGrid
+    keys, vox = grid.export_blocks(device=True)
+    n_halo = 0 if halo_keys is None else int(halo_keys.shape[0])
+    tmp = VoxelBlockGrid(voxel_size=grid.voxel_size, truncation=grid.truncation,
+                         max_weight=grid.max_weight,
+                         capacity=max(1024, 2 * (int(keys.shape[0]) + n_halo)))
+    tmp.import_blocks(keys, vox)
+    if n_halo:
+        tmp.import_blocks(halo_keys, halo_vox)
+    nat.call("rk_grid_set_shard", tmp._ensure(), int(rank), int(world))
+    return extract_mesh_device(tmp, min_weight)
+
+
+def merge_meshes(parts):
+    """Concatenate per-rank (V, T, N) meshes and merge vertices that sit at
+    the same exact position (edges on shard boundaries are produced by both
+    neighbouring ranks).  Returns host (V, T, N)."""
+    Vs = [np.asarray(nat.to_host(v) if nat.is_tensor(v) else v, dtype=np.float64).reshape(-1, 3)
+          for v, _, _ in parts]
+    Ts, Ns, base = [], [], 0
+    for (v, t, n), V in zip(parts, Vs):
+        T = np.asarray(nat.to_host(t) if nat.is_tensor(t) else t, dtype=np.int64).reshape(-1, 3)
+        Ts.append(T + base)
+        Ns.append(np.asarray(nat.to_host(n) if nat.is_tensor(n) else n, dtype=np.float64).reshape(-1, 3))
+        base += V.shape[0]
+    V = np.concatenate(Vs) if Vs else np.zeros((0, 3))
+    N = np.concatenate(Ns) if Ns else np.zeros((0, 3))
+    T = np.concatenate(Ts) if Ts else np.zeros((0, 3), np.int64)
+    if V.shape[0] == 0:
+        return V, T.astype(np.int32), N
+    uniq, first, inv = np.unique(V, axis=0, return_index=True, return_inverse=True)
+    return uniq, inv.reshape(-1)[T].astype(np.int32), N[first]

@@ -264,32 +264,34 @@ class VoxelBlockGrid:
                  nat.stream_ptr())
         return nat.to_host(out[:n.value])
 
-    def export_blocks(self):
+    def export_blocks(self, device: bool = False):
         """Every stored block in sorted-key order, read back in one device
         call: (keys (n,3) int32, voxels (n,4096,2) float32 {tsdf, weight}) --
-        the SDFG snapshot's payload (io_formats.py:267-277)."""
+        the SDFG snapshot's payload (io_formats.py:267-277).  device=True
+        returns CUDA tensors (for collectives) instead of numpy arrays."""
         self._prepare()
         keys = self._export_keys(touched=False)
-        if keys.shape[0] == 0:
-            return keys.reshape(0, 3), np.zeros((0, BLOCK_VOXELS, 2), np.float32)
-        keys = keys[np.lexsort((keys[:, 2], keys[:, 1], keys[:, 0]))]
-        kd = nat.to_dev(keys, np.int32)
+        if keys.shape[0]:
+            keys = keys[np.lexsort((keys[:, 2], keys[:, 1], keys[:, 0]))]
+        kd = nat.to_dev(keys.reshape(-1, 3), np.int32)
         vox = nat.empty((keys.shape[0], BLOCK_VOXELS, 2), np.float32)
-        nat.call("rk_grid_read_blocks", self._handle, nat.ptr(kd), keys.shape[0], nat.ptr(vox), None,
-                 nat.stream_ptr())
-        return keys, nat.to_host(vox)
+        if keys.shape[0]:
+            nat.call("rk_grid_read_blocks", self._handle, nat.ptr(kd), keys.shape[0], nat.ptr(vox),
+                     None, nat.stream_ptr())
+        if device:
+            return kd, vox
+        return keys.reshape(-1, 3), nat.to_host(vox)
 
     def import_blocks(self, keys, voxels):
         """Insert / overwrite whole blocks in one device call (keys (n,3),
-        voxels (n,4096,2) {tsdf, weight})."""
-        keys = np.ascontiguousarray(np.asarray(keys, dtype=np.int32).reshape(-1, 3))
-        n = keys.shape[0]
+        voxels (n,4096,2) {tsdf, weight}; numpy arrays or CUDA tensors)."""
+        n = int(keys.shape[0])
         if n == 0:
             return
         self._prepare()
         self._ensure_capacity(self.info()[0] + n)
-        kd = nat.to_dev(keys, np.int32)
-        vd = nat.to_dev(np.asarray(voxels, dtype=np.float32).reshape(n, BLOCK_VOXELS, 2), np.float32)
+        kd = nat.to_dev(keys, np.int32).reshape(n, 3).contiguous()
+        vd = nat.to_dev(voxels, np.float32).reshape(n, BLOCK_VOXELS, 2).contiguous()
         nat.call("rk_grid_write_blocks", self._handle, nat.ptr(kd), n, nat.ptr(vd), nat.stream_ptr())
         self.blocks._bump()
 

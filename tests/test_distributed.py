@@ -123,6 +123,53 @@ def test_sharded_pairs_gather_in_order_gloo():
     assert out[0] == out[1] == [0.5 * i for i in range(37)]
 
 
+def test_halo_plan_selects_exactly_the_foreign_neighbours():
+    g = np.random.default_rng(3)
+    keys = np.unique(g.integers(-4, 5, size=(300, 3)), axis=0)
+    owner = np.arange(len(keys)) % 3
+    by_rank = [keys[owner == r] for r in range(3)]
+    plan = rkd.halo_plan(by_rank)
+    for s_ in range(3):
+        for r in range(3):
+            got = {tuple(k) for k in by_rank[r][plan[r][s_]].tolist()}
+            if r == s_:
+                assert not got
+                continue
+            want = {tuple(k) for k in by_rank[r].tolist()
+                    if np.any(np.abs(by_rank[s_] - np.array(k)).max(axis=1) == 1)}
+            assert got == want
+
+
+def test_merge_meshes_dedups_shared_boundary_vertices():
+    V0 = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    V1 = np.array([[1.0, 0, 0], [0, 1, 0], [1, 1, 0]])       # two vertices shared with V0
+    T0, T1 = np.array([[0, 1, 2]]), np.array([[0, 2, 1]])
+    N0, N1 = np.tile([0, 0, 1.0], (3, 1)), np.tile([0, 0, 1.0], (3, 1))
+    V, T, N = rkd.merge_meshes([(V0, T0, N0), (V1, T1, N1)])
+    assert V.shape == (4, 3) and T.shape == (2, 3)
+    tris = {tuple(sorted(map(tuple, V[t].tolist()))) for t in T}
+    assert tris == {tuple(sorted(map(tuple, V0.tolist()))), tuple(sorted(map(tuple, V1.tolist())))}
+
+
+def _halo_exchange_job(rank, world):
+    """The all-to-all of halo keys as ShardedGrid.extract_mesh does it (CPU)."""
+    keys = np.array([[x, 0, 0] for x in range(6)])
+    mine = keys[np.arange(6) % world == rank]
+    allk = [keys[np.arange(6) % world == q] for q in range(world)]
+    plan = rkd.halo_plan(allk)
+    send = torch.from_numpy(np.concatenate([mine[plan[rank][s_]] for s_ in range(world)]).astype(np.int32))
+    out_split = [int(plan[q][rank].size) for q in range(world)]
+    in_split = [int(plan[rank][s_].size) for s_ in range(world)]
+    recv = torch.empty((sum(out_split), 3), dtype=torch.int32)
+    torch.distributed.all_to_all_single(recv, send, out_split, in_split)
+    return sorted(recv[:, 0].tolist())
+
+
+def test_halo_exchange_gloo():
+    out = run_ranks(_halo_exchange_job)
+    assert out[0] == [1, 3, 5] and out[1] == [0, 2, 4]     # x-neighbours owned by the other rank
+
+
 def test_block_owner_partitions_keys(golden_tsdf):
     keys = golden_tsdf["street_keys"]
     for world in (2, 4, 8):

@@ -541,6 +541,47 @@ def test_sharded_batched_sequence_equals_single_grid(rk, sensors):
     assert np.array_equal(k[order], kf) and np.array_equal(v[order], vf)
 
 
+def test_sharded_mesh_with_halo_equals_single_grid(rk, sensors):
+    """Distributed marching cubes (two shards emulated in one process): each
+    shard meshes its own blocks with the other's boundary blocks as halo; the
+    merged mesh equals the single-grid mesh (same vertex positions, same
+    triangles up to relabelling)."""
+    import torch
+    from paper_2112_02779_b200 import _native as nat
+    from paper_2112_02779_b200 import distributed as rkd
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = sensors["ouster"]
+    traj = scenes.street_trajectory(3, seed=0)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    poses = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    inv = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).cuda()
+    full = rk.VoxelBlockGrid(voxel_size=0.1, capacity=4096)
+    pipeline.integrate_sequence(full, intr, frames, poses, inv, clip_max=30.0)
+    ref = rk.extract_mesh(full)
+    keys, vox = full.export_blocks(device=True)
+    owner = torch.from_numpy(rkd.block_owner(nat.to_host(keys), 2)).cuda()
+    shards = []
+    for r in range(2):
+        g = rk.VoxelBlockGrid(voxel_size=0.1, capacity=4096)
+        m = owner == r
+        g.import_blocks(keys[m], vox[m])
+        shards.append(g)
+    by_rank = [s.export_blocks(device=True) for s in shards]
+    plan = rkd.halo_plan([nat.to_host(k) for k, _ in by_rank])
+    parts = []
+    for r in range(2):
+        o = 1 - r
+        sel = torch.from_numpy(plan[o][r]).cuda()
+        parts.append(rkd.mesh_from_shard(shards[r], r, 2, by_rank[o][0][sel], by_rank[o][1][sel]))
+    V, T, N = rkd.merge_meshes(parts)
+    assert V.shape[0] == ref.n_vertices and T.shape[0] == ref.n_triangles > 1000
+    pos = {tuple(p): i for i, p in enumerate(ref.vertices.tolist())}
+    remap = np.array([pos[tuple(p)] for p in V.tolist()])
+    assert np.abs(N - ref.normals[remap]).max() < 1e-12
+    canon = lambda tris: {tuple(np.roll(t, -int(np.argmin(t)))) for t in tris.tolist()}  # noqa: E731
+    assert canon(remap[T]) == canon(ref.triangles)
+
+
 def test_integrate_rejects_bad_pose(rk, sensors, golden_icp):
     grid = rk.VoxelBlockGrid(voxel_size=0.1)
     img = rk.RangeImage(golden_icp["synth/dst"], sensors["synth"])
