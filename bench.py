@@ -266,17 +266,36 @@ def run_ours(args, rank, world, dist):
     tsdf_achieved = tsdf_bytes / (acc["tsdf"] / K / 1e3) / 1e9
     coarse = len({s for s, _ in cfg.schedule if s > 1})
     launches = K * (1 + coarse + 1 + pipeline.LAUNCHES_CLEAR + pipeline.LAUNCHES_PER_FRAME * args.frames)
+    # single-pair latency through the public API (host numpy in, pose out):
+    # the online-odometry use (the paper's "registration at 100 Hz")
+    latency = None
+    if dist is None:
+        src0 = D["src"][D["pair_idx"][0]].cpu().numpy()
+        dst0 = D["dst"][D["pair_idx"][0]].cpu().numpy()
+        for _ in range(3):
+            rk.register(rk.RangeImage(src0, intr), rk.RangeImage(dst0, intr))
+        torch.cuda.synchronize()
+        t_l = time.perf_counter()
+        n_l = 20
+        for _ in range(n_l):
+            res1 = rk.register(rk.RangeImage(src0, intr), rk.RangeImage(dst0, intr))
+        latency = {"ms": 1e3 * (time.perf_counter() - t_l) / n_l, "iterations": len(res1.stats),
+                   "what": "register() of one 64x1024 pair from host arrays: H2D, K1 normals, "
+                           "K3 schedule, pose D2H"}
     # K6 on the sequence's final grid (outside the timed region), wall clock
     # incl. its syncs: extract_mesh through the public API on one GPU; at N > 1
     # the distributed form (halo all-to-all, per-shard MC, mesh gather + merge)
     if dist is None:
         from paper_2112_02779_b200.mesh_extract import extract_mesh_device
         extract_mesh_device(grid)
-        torch.cuda.synchronize()
-        t_mc = time.perf_counter()
-        v, tri, _ = extract_mesh_device(grid)
-        torch.cuda.synchronize()
-        mesh = {"ms": 1e3 * (time.perf_counter() - t_mc), "vertices": int(v.shape[0]),
+        mc_ms = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t_mc = time.perf_counter()
+            v, tri, _ = extract_mesh_device(grid)
+            torch.cuda.synchronize()
+            mc_ms.append(1e3 * (time.perf_counter() - t_mc))
+        mesh = {"ms": float(np.median(mc_ms)), "vertices": int(v.shape[0]),
                 "triangles": int(tri.shape[0]), "blocks": int(n_blocks)}
     else:
         tsdf.sharded.extract_mesh()
@@ -294,7 +313,7 @@ def run_ours(args, rank, world, dist):
                 upd_local=upd_local,
                 tsdf_achieved=tsdf_achieved, tsdf_updated=upd_per_step, n_blocks=n_blocks,
                 clocks=clocks.summary(), launches=launches, ok_frac=ok_frac, D=D, tsdf=tsdf, cfg=cfg,
-                mesh=mesh)
+                mesh=mesh, latency=latency)
 
 
 def run_e2e(args, rank, world, dist, D, tsdf, cfg):
@@ -545,6 +564,7 @@ def main():
                      "tsdf_sequence": r["tsdf_ms"] / args.steps},
         "gt_recovered_frac": r["ok_frac"],
         "marching_cubes": r["mesh"],
+        "single_pair_latency": r["latency"],
         "clocks": r["clocks"], "gpu_launches": r["launches"],
         "e2e": e2e, "cpu_baseline": cpu,
     }

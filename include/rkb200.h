@@ -279,8 +279,10 @@ int rk_grid_query(rk_grid* g, const double* pts, int64_t n, double* sdf, double*
 
 /* ------------------------------------------------------------ marching cubes
  * extract_mesh  mesh_extract.py:85-209 over every stored block.  tri_table:
- * device (256,16) int8 TRI_TABLE (mc_tables.py:114).  The mesh lives on the
- * device until rk_mesh_copy()/rk_mesh_free(); counts = {vertices, triangles}. */
+ * device (256,16) int8 TRI_TABLE (mc_tables.py:114).  The mesh lives in the
+ * grid's grow-only scratch: valid until the next rk_mc_extract on that grid
+ * (copy it out with rk_mesh_copy); rk_mesh_free releases the handle only.
+ * counts = {vertices, triangles}. */
 typedef struct rk_mesh rk_mesh;
 int rk_mc_extract(rk_grid* g, const int8_t* tri_table, float min_weight, rk_mesh** out,
                   void* stream);

@@ -316,10 +316,12 @@ __global__ void k_mc_normalize(Mesh m, long long nv) {
 }  // namespace
 
 // --------------------------------------------------------------- host side
+// The mesh lives in a grow-only scratch owned by the grid (rk_grid_scratch_):
+// valid until the next rk_mc_extract on the same grid or its destruction; no
+// cudaMalloc / cudaFree (device-wide synchronisations) per extraction.
 struct rk_mesh {
   Mesh m;
   long long nv, nt;
-  void* blob;
 };
 
 
@@ -329,12 +331,12 @@ extern "C" int rk_mc_extract(rk_grid* grid, const int8_t* tri_table, float min_w
   GridView g;
   int rc = rk_grid_view_(grid, &g);
   if (rc) return rc;
+  unsigned long long* ctr =
+      static_cast<unsigned long long*>(rk_grid_scratch_(grid, 1, 8 * sizeof(unsigned long long)));
+  if (!ctr) return RK_ECUDA;
+  RK_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st));
   rk_mesh* mesh = new rk_mesh();
   mesh->nv = mesh->nt = 0;
-  mesh->blob = nullptr;
-  unsigned long long* ctr = nullptr;
-  RK_CUDA(cudaMalloc(&ctr, 8 * sizeof(unsigned long long)));
-  RK_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st));
   unsigned long long h_ctr[8] = {0};
   if (g.n_blocks > 0) {
     k_mc_count<<<(unsigned)g.n_blocks, 256, 0, st>>>(g, tri_table, min_weight, ctr);
@@ -349,9 +351,11 @@ extern "C" int rk_mc_extract(rk_grid* grid, const int8_t* tri_table, float min_w
   while (hcap < (unsigned long long)vcap * 2ull) hcap <<= 1;
   size_t bytes = hcap * (sizeof(unsigned long long) + sizeof(int32_t)) + vcap * 6 * sizeof(double) +
                  tcap * 3 * sizeof(int32_t) + 1024;
-  char* blob = nullptr;
-  RK_CUDA(cudaMalloc(&blob, bytes));
-  mesh->blob = blob;
+  char* blob = static_cast<char*>(rk_grid_scratch_(grid, 0, bytes));
+  if (!blob) {
+    delete mesh;
+    return RK_ECUDA;
+  }
   Mesh& m = mesh->m;
   m.vkeys = reinterpret_cast<unsigned long long*>(blob);
   m.vids = reinterpret_cast<int32_t*>(m.vkeys + hcap);
@@ -374,8 +378,6 @@ extern "C" int rk_mc_extract(rk_grid* grid, const int8_t* tri_table, float min_w
   RK_CUDA(cudaStreamSynchronize(st));
   if (h_ctr[4]) {
     rk_set_error("marching cubes output overflow");
-    cudaFree(blob);
-    cudaFree(ctr);
     delete mesh;
     return RK_ECAPACITY;
   }
@@ -407,10 +409,6 @@ extern "C" int rk_mesh_copy(rk_mesh* mesh, double* verts, double* normals, int32
 }
 
 extern "C" int rk_mesh_free(rk_mesh* mesh) {
-  if (!mesh) return RK_OK;
-  cudaDeviceSynchronize();
-  cudaFree(mesh->blob);
-  cudaFree(mesh->m.counters);
-  delete mesh;
+  delete mesh;  // the buffers belong to the grid's scratch
   return RK_OK;
 }

@@ -582,7 +582,28 @@ struct rk_grid {
   const long long* global_touch = nullptr;  // device {count, max key} (sharded grids)
   cudaStream_t side = nullptr;               // activation stream of rk_grid_integrate_frames
   cudaEvent_t ev_act[2] = {nullptr, nullptr}, ev_int[2] = {nullptr, nullptr}, ev_fork = nullptr;
+  void* scratch[2] = {nullptr, nullptr};     // rk_grid_scratch_ (marching cubes output)
+  size_t scratch_bytes[2] = {0, 0};
 };
+
+void* rk_grid_scratch_(rk_grid* g, int which, size_t bytes) {
+  if (bytes > g->scratch_bytes[which]) {
+    if (g->scratch[which]) {
+      cudaDeviceSynchronize();  // earlier users of the slot may still be running
+      cudaFree(g->scratch[which]);
+      g->scratch[which] = nullptr;
+      g->scratch_bytes[which] = 0;
+    }
+    const size_t want = bytes + bytes / 4;  // headroom: meshes grow with the grid
+    cudaError_t e = cudaMalloc(&g->scratch[which], want);
+    if (e != cudaSuccess) {
+      rk_cuda_status(e, "rk_grid_scratch_");
+      return nullptr;
+    }
+    g->scratch_bytes[which] = want;
+  }
+  return g->scratch[which];
+}
 
 // the grid as seen by the kernels of one touched-set slot
 static GridDev view(const rk_grid* g, int slot) {
@@ -686,6 +707,8 @@ extern "C" int rk_grid_destroy(rk_grid* g) {
   free_tables(g->d);
   cudaFree(g->d.ctr);
   cudaFree(g->d.tc);
+  cudaFree(g->scratch[0]);
+  cudaFree(g->scratch[1]);
   if (g->side) {
     cudaStreamDestroy(g->side);
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(g->ev_act[i]); cudaEventDestroy(g->ev_int[i]); }
