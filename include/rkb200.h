@@ -112,14 +112,16 @@ int rk_normals_pca(const rk_sensor* s, const float* range, int32_t batch, int32_
 int rk_zbuffer_image(const rk_sensor* s, const double* u, const int32_t* v, const double* r,
                      const int8_t* status, int64_t n, float* range_out, int64_t* stats4,
                      unsigned long long* zwork, void* stream);
-/* rk_normals_cross's surfel map as a pyramid of 32-byte records per pixel
- * ({nx, ny, nz, range-if-valid}, {association target r*dir32 + origin32, 0}):
- * per image, the full map (H*W records) followed by the decimated map of
- * every stride in strides_host that is > 1 (ceil(H/s) x ceil(W/s), pixel
- * (i, j) = full (i*s, j*s)), in order; pitch (in records) = H*W + sum of the
- * decimated sizes.  The registration's coarse levels gather from compact
- * maps, and every level reads its target from the record instead of the
- * sensor's ray tables. */
+/* rk_normals_cross's surfel map as a pyramid of per-pixel records, per
+ * image: the full map (H*W records) followed by the decimated map of every
+ * stride in strides_host that is > 1 (ceil(H/s) x ceil(W/s), pixel (i, j) =
+ * full (i*s, j*s)), in order; pitch (in records) = H*W + sum of the decimated
+ * sizes.  The registration's coarse levels gather from compact maps.  A
+ * record is rk_surfel_record_floats() floats: 4 = {nx, ny, nz,
+ * range-if-valid} (default build; the association target is formed from the
+ * sensor's shared float32 ray tables), 8 = that plus {target r*dir32 +
+ * origin32, 0} (RK_SURFEL_REC=32 builds). */
+int rk_surfel_record_floats(void);
 int rk_normals_cross_pyramid(const rk_sensor* s, const float* range, int32_t batch,
                              const int32_t* strides_host, int32_t n_strides, float* surfel_pyr,
                              int64_t pitch, void* stream);

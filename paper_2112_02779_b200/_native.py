@@ -56,6 +56,7 @@ SIGNATURES = {
     "rk_normals_cross": [_p, _p, _i32, _p, _p, _p, _p],
     "rk_stride_compact": [_p, _p, _i32, _i32, _f32, _f32, _p, _p, _p],
     "rk_normals_cross_pyramid": [_p, _p, _i32, _p, _i32, _p, _i64, _p],
+    "rk_surfel_record_floats": [],
     "rk_normals_pca": [_p, _p, _i32, _i32, _f64, _f64, _p, _p, _p, _p],
     "rk_zbuffer_image": [_p, _p, _p, _p, _p, _i64, _p, _p, _p, _p],
     "rk_unproject_pixels": [_p, _p, _p, _p, _i64, _p, _p],

@@ -327,8 +327,15 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
   const int flat = row * s.W + col;
   constexpr bool FUSED = RK_ICP_FUSED && MATH == MATH_FAST;
   float4 n, q;
-  if (lvl_rec) {
-    // surfel pyramid: 32-byte {n, range} + {target} records; the level's
+  if (lvl_rec && RK_SURFEL_REC == 16) {
+    // 16-byte pyramid records {n, range}; the target from the shared ray tables
+    n = __ldg(surf + (lvl_w ? lvl_off + ri * lvl_w + ci : flat));
+    const float4 d = __ldg(s.dirs32 + flat);
+    const float4 o = __ldg(s.origins32 + col);
+    q = make_float4(__fadd_rn(__fmul_rn(n.w, d.x), o.x), __fadd_rn(__fmul_rn(n.w, d.y), o.y),
+                    __fadd_rn(__fmul_rn(n.w, d.z), o.z), 0.f);
+  } else if (lvl_rec) {
+    // RK_SURFEL_REC=32 pyramid: {n, range} + {target} records; the level's
     // compact decimated map (lvl_w > 0) or the full map (level stride 1)
     const int idx = lvl_w ? lvl_off + ri * lvl_w + ci : flat;
     n = __ldg(surf + 2 * idx);
@@ -376,10 +383,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   const int H = s.H, W = s.W;
   const size_t HW = (size_t)H * W;
   const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
-  // a surfel pyramid (surfel_pitch != 0) holds 32-byte records {n, range},
+  // a surfel pyramid (surfel_pitch != 0) holds RK_SURFEL_REC-byte records {n, range}(, {target});
   // {target}; a plain surfel map 16-byte {n, range}
   const bool rec = A.cfg.surfel_pitch != 0;
-  const long long surf_pitch = rec ? 2 * A.cfg.surfel_pitch : (long long)HW;
+  const long long surf_pitch = rec ? (RK_SURFEL_REC / 16) * A.cfg.surfel_pitch : (long long)HW;
   const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * surf_pitch;
 
   __shared__ double sh_pose[GROUPS][12];

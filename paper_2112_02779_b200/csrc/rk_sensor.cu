@@ -437,7 +437,11 @@ __global__ void __launch_bounds__(K1_THREADS) k_normals_cross(
     }
     if (valid) valid[i] = ok ? 1 : 0;
     if (surfel) {
-      if (targets) {
+      if (targets && RK_SURFEL_REC == 16) {
+        // 16-byte pyramid records {n, range}: the registration forms the
+        // target from the (L2-resident, shared) float32 ray tables
+        surfel[img * surfel_pitch + p] = make_float4(n0, n1, n2, ok ? r0 : 0.f);
+      } else if (targets) {
         // pyramid layout: {n, range} then the association target
         // r * dir32 + origin32 with the reference's separate roundings
         // (registration.py:168-176), so the registration gathers one
@@ -472,10 +476,15 @@ __global__ void k_surfel_decimate(int H, int W, int batch, float4* pyr, int64_t 
     const int64_t img = k / per;
     const int q = (int)(k - img * per);
     const int i = q / Ws, j = q - i * Ws;
-    float4* base = pyr + 2 * img * pitch;  // 2 float4 records (see k_normals_cross)
     const int64_t from = (int64_t)i * stride * W + (int64_t)j * stride;
-    base[2 * (off + q)] = base[2 * from];
-    base[2 * (off + q) + 1] = base[2 * from + 1];
+    if (RK_SURFEL_REC == 16) {
+      float4* base = pyr + img * pitch;
+      base[off + q] = base[from];
+    } else {
+      float4* base = pyr + 2 * img * pitch;  // 2 float4 records (see k_normals_cross)
+      base[2 * (off + q)] = base[2 * from];
+      base[2 * (off + q) + 1] = base[2 * from + 1];
+    }
   }
 }
 
@@ -488,6 +497,8 @@ extern "C" int rk_normals_cross(const rk_sensor* s, const float* range, int32_t 
   RK_LAUNCHED("k_normals_cross");
   return RK_OK;
 }
+
+extern "C" int rk_surfel_record_floats(void) { return RK_SURFEL_REC / 4; }
 
 extern "C" int rk_normals_cross_pyramid(const rk_sensor* s, const float* range, int32_t batch,
                                         const int32_t* strides_host, int32_t n_strides,

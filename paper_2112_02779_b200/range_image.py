@@ -317,9 +317,10 @@ def normals_cross(img: RangeImage) -> NormalImage:
 @dataclass
 class SurfelPyramid:
     """Per image: the full surfel map followed by the decimated map of every
-    coarse stride (rk_normals_cross_pyramid), as 32-byte records {nx, ny,
-    nz, range-if-valid} {target x, y, z, 0}; ``offsets`` maps stride -> pixel
-    offset inside an image's ``pitch``-pixel block (stride 1 -> 0)."""
+    coarse stride (rk_normals_cross_pyramid), as 16-byte records {nx, ny,
+    nz, range-if-valid} (32-byte builds append {target x, y, z, 0});
+    ``offsets`` maps stride -> pixel offset inside an image's ``pitch``-pixel
+    block (stride 1 -> 0)."""
 
     data: object
     pitch: int
@@ -344,7 +345,7 @@ def normals_cross_batch(intr: LidarIntrinsics, ranges, strides=None):
         offsets[s] = off
         off += -(-H // s) * -(-W // s)
     pitch = off
-    data = nat.empty((B, pitch, 8), np.float32)
+    data = nat.empty((B, pitch, nat.load().rk_surfel_record_floats()), np.float32)
     st = np.asarray(coarse, dtype=np.int32)
     nat.call("rk_normals_cross_pyramid", lm.device_sensor(intr), nat.ptr(ranges), B,
              st.ctypes.data if st.size else None, int(st.size), nat.ptr(data), int(pitch),

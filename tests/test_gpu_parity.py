@@ -284,13 +284,18 @@ def test_register_batch_surfel_pyramid_bitidentical(rk, pair, sensors, golden_ic
     assert isinstance(pyr, SurfelPyramid) and set(pyr.offsets) == {1, 2, 3, 4}
     HW = intr.height * intr.width
     assert torch.equal(pyr.data[:, :HW, :4].reshape(flat.shape), flat)
-    # the record's target is the reference's float32 r * dir32 + origin32 (registration.py:168-176)
-    d32 = np.stack(intr.ray_tables_flat_f32[0], -1)
-    o32 = np.stack(intr.ray_tables_flat_f32[1], -1)
-    r = g[f"{pair}/dst"].reshape(-1).astype(np.float32)
-    tgt = r[:, None] * d32 + o32[np.arange(HW) % intr.width]
-    got = pyr.data[0, :HW, 4:7].cpu().numpy()
-    assert np.array_equal(got[r > 0], tgt[r > 0])
+    if pyr.data.shape[-1] == 8:  # RK_SURFEL_REC=32 builds carry the target
+        # the record's target is the reference's float32 r * dir32 + origin32 (registration.py:168-176)
+        d32 = np.stack(intr.ray_tables_flat_f32[0], -1)
+        o32 = np.stack(intr.ray_tables_flat_f32[1], -1)
+        r = g[f"{pair}/dst"].reshape(-1).astype(np.float32)
+        tgt = r[:, None] * d32 + o32[np.arange(HW) % intr.width]
+        got = pyr.data[0, :HW, 4:7].cpu().numpy()
+        assert np.array_equal(got[r > 0], tgt[r > 0])
+    for s, off in pyr.offsets.items():  # decimated maps = the strided full map
+        Hs, Ws = -(-intr.height // s), -(-intr.width // s)
+        lvl = pyr.data[:, off:off + Hs * Ws, :4].reshape(3, Hs, Ws, 4)
+        assert torch.equal(lvl, flat[:, ::s, ::s])
     a = rk.register_batch(intr, src, dst, flat, config=cfg, with_stats=True)
     b = rk.register_batch(intr, src, dst, pyr, config=cfg, with_stats=True)
     assert torch.equal(a.poses, b.poses) and torch.equal(a.iterations, b.iterations)
