@@ -3,6 +3,10 @@ CLI runs in Python loops (cli.py:248-328 odometry / eval-reg pair sweeps,
 cli.py:267-283 integrate) expressed as a few launches over device buffers.
 
 * ``render_batch``   -- synthetic inputs on the device (synth.py:108-134, N4)
+* ``odometry``       -- cli.py:248-263 frame-to-frame registration of a whole
+  sequence as ONE register_batch launch + the host pose prefix product
+* ``odometry_integrate`` -- C2 end to end: odometry, then the sequence
+  integrated at the estimated poses
 * ``integrate_sequence`` -- activate + integrate F posed frames into one grid
   with no host synchronisation between frames
 * ``shard`` / ``gather_poses`` -- one-process-per-GPU partitioning of
@@ -18,6 +22,8 @@ from .trace import nvtx
 from . import lidar_model as lm
 from .distributed import all_gather_varsize, shard  # noqa: F401  (re-exported)
 from .sdf_volume import VoxelBlockGrid
+from .range_image import RangeImage, normals_cross_batch, to_point_cloud
+from .registration import RegistrationConfig, initial_translation_by_centroids, register_batch
 from .se3 import RigidTransform
 
 _KIND = {"plane": 0, "sphere": 1, "box": 2}
@@ -117,6 +123,61 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
         g.replay()
     grid.blocks._bump()
     return updated
+
+
+@nvtx("odometry")
+def odometry(intr: lm.LidarIntrinsics, frames, config: RegistrationConfig = RegistrationConfig(),
+             init: str = "identity", with_stats: bool = False):
+    """Frame-to-frame odometry over a (F, H, W) float32 device sequence
+    (cli.py:248-263 ``cmd_odometry``): frame k is registered to frame k-1
+    from the identity (or, init="centroid", the centroid translation of the
+    two clouds, cli.py:257-258) and world_k = world_{k-1} @ pose_k, world_0 =
+    identity.  The F-1 pairs are independent, so they run as
+    ONE register_batch launch over a surfel pyramid of the sequence; only the
+    prefix product runs on the host, with the reference's own numpy
+    composition (se3.py:69-71), so the chain rounds exactly as cmd_odometry's.
+
+    Returns (world poses: list of F RigidTransform, BatchResult of the F-1
+    relative registrations, or None when F < 2).
+    """
+    t = nat.torch()
+    F = int(frames.shape[0])
+    if init not in ("identity", "centroid"):
+        raise ValueError("init must be 'identity' or 'centroid'")
+    world = [RigidTransform.identity()]
+    if F < 2:
+        return world, None
+    frames = frames.contiguous()
+    dev = nat.device()
+    pair_src = t.arange(1, F, dtype=t.int32, device=dev)
+    pair_dst = t.arange(0, F - 1, dtype=t.int32, device=dev)
+    inits = None
+    if init == "centroid":
+        clouds = [to_point_cloud(RangeImage(frames[k], intr)) for k in range(F)]
+        inits = nat.to_dev(np.stack([initial_translation_by_centroids(clouds[k], clouds[k - 1]).as_row12()
+                                     for k in range(1, F)]), np.float64)
+    surf = normals_cross_batch(intr, frames, strides=[s for s, _ in config.schedule])
+    res = register_batch(intr, frames, frames, surf, pair_src, pair_dst, inits, config,
+                         with_stats=with_stats)
+    rel = nat.to_host(res.poses)
+    for k in range(F - 1):
+        world.append(world[-1] @ RigidTransform(rel[k, :9].reshape(3, 3), rel[k, 9:]))
+    return world, res
+
+
+@nvtx("odometry_integrate")
+def odometry_integrate(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames,
+                       config: RegistrationConfig = RegistrationConfig(), init: str = "identity",
+                       clip_min: float = 0.0, clip_max: float = np.inf, graph: bool = False):
+    """C2 end to end (cli.py:248-283 odometry then integrate): estimate the
+    sequence's trajectory and integrate every frame at its estimated pose.
+    Returns (world poses, BatchResult, device int64 updated-voxel counter)."""
+    world, res = odometry(intr, frames, config, init)
+    poses_w = nat.to_dev(poses_to_rows(world), np.float64)
+    inv_w = nat.to_dev(np.stack([p.inverse().as_row12() for p in world]), np.float64)
+    updated = integrate_sequence(grid, intr, frames, poses_w, inv_w, clip_min=clip_min,
+                                 clip_max=clip_max, graph=graph)
+    return world, res, updated
 
 
 # launches issued per call (the bench's gpu_launches accounting)
