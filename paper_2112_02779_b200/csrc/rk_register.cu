@@ -43,6 +43,12 @@ static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p)
 namespace {
 
 constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
+// RK_ICP_LVL_SMEM: the per-level constants (gate^2, 1/k, 1/s, stride, surfel
+// level offset/width) live in shared memory, so under the 64-register cap the
+// compiler re-reads them with one LDS instead of re-deriving them per point
+#ifndef RK_ICP_LVL_SMEM
+#define RK_ICP_LVL_SMEM 1
+#endif
 #ifndef RK_ICP_THREADS
 #define RK_ICP_THREADS 256
 #endif
@@ -395,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   __shared__ int sh_cnt[NW];
   __shared__ int sh_ctrl[GROUPS];
   __shared__ float sh_pose32[GROUPS][12];
+  __shared__ float4 sh_lvl[GROUPS][2];  // RK_ICP_LVL_SMEM: {gate2, 1/k, 1/s, stride}, {level off, level w}
   if (gtid < 12) sh_pose[g][gtid] = A.init12[pair * 12 + gtid];
   int n_done = 0, status = RK_ICP_CONVERGED;
 #if RK_ICP_TIME_SOLVE
@@ -426,6 +433,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     const int lvl_off = A.cfg.surfel_pitch ? A.cfg.surfel_level_off[lv] : 0;
     const int lvl_w = (A.cfg.surfel_pitch && lvl_off > 0) ? Ws : 0;
     const int row_step = stride * W;
+    if (RK_ICP_LVL_SMEM && gtid == 0) {
+      sh_lvl[g][0] = make_float4(gate2, inv_k, inv_s, __int_as_float(stride));
+      sh_lvl[g][1] = make_float4(__int_as_float(lvl_off), __int_as_float(lvl_w), 0.f, 0.f);
+    }
     // executed work (the roofline's unit) = valid points of this level x the
     // iterations run; counted once per level, outside the hot loop
     unsigned valid_lv = 0;
@@ -480,8 +491,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
             if (!range_ok(r, cmin, cmax)) continue;
             float mx, my, mz;
             move_f32(P, r, d4, o4, mx, my, mz);
-            associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, stride, lvl_off, lvl_w, inv_s,
-                                               gate2, inv_k, acc, cost, sumsq, cnt);
+            if (RK_ICP_LVL_SMEM) {
+              const float4 L0 = sh_lvl[g][0], L1 = sh_lvl[g][1];
+              associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, __float_as_int(L0.w),
+                                                 __float_as_int(L1.x), __float_as_int(L1.y), L0.z, L0.x,
+                                                 L0.y, acc, cost, sumsq, cnt);
+            } else {
+              associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, stride, lvl_off, lvl_w, inv_s,
+                                                 gate2, inv_k, acc, cost, sumsq, cnt);
+            }
           }
         }
       } else if (F32X) {
