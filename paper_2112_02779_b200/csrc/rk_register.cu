@@ -49,6 +49,15 @@ constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
 #ifndef RK_ICP_LVL_SMEM
 #define RK_ICP_LVL_SMEM 1
 #endif
+// RK_ICP_PREFETCH: after a point's gather, prefetch the records one view row
+// below it (1 = into L1, 2 = into L2): the column walk's next point projects
+// close to there, so its dependent gather finds the line on chip
+#ifndef RK_ICP_PREFETCH
+#define RK_ICP_PREFETCH 1
+#endif
+#ifndef RK_ICP_PF_ROWS
+#define RK_ICP_PF_ROWS 1  // how many view rows ahead (1..3 measured equal)
+#endif
 #ifndef RK_ICP_THREADS
 #define RK_ICP_THREADS 256
 #endif
@@ -288,6 +297,11 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
                                                 float gate2, float inv_k, float* acc, float& cost,
                                                 float& sumsq, int& cnt);
 
+__device__ __forceinline__ void prefetch_line(const void* p) {
+  if (RK_ICP_PREFETCH == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  if (RK_ICP_PREFETCH == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // float32 unprojection r * dir + origin and rigid move R p + t (FMA chains),
 // P = {R row-major, t} in float32
 __device__ __forceinline__ void move_f32(const float* P, float r, const float4& d, const float4& o,
@@ -335,9 +349,14 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
   float4 n, q;
   if (lvl_rec && RK_SURFEL_REC == 16) {
     // 16-byte pyramid records {n, range}; the target from the shared ray tables
-    n = __ldg(surf + (lvl_w ? lvl_off + ri * lvl_w + ci : flat));
+    const int idx = lvl_w ? lvl_off + ri * lvl_w + ci : flat;
+    n = __ldg(surf + idx);
     const float4 d = __ldg(s.dirs32 + flat);
     const float4 o = __ldg(s.origins32 + col);
+    if (RK_ICP_PREFETCH && row + RK_ICP_PF_ROWS * stride < s.H) {
+      prefetch_line(surf + (lvl_w ? idx + RK_ICP_PF_ROWS * lvl_w : flat + RK_ICP_PF_ROWS * stride * s.W));
+      prefetch_line(s.dirs32 + flat + RK_ICP_PF_ROWS * stride * s.W);
+    }
     q = make_float4(__fadd_rn(__fmul_rn(n.w, d.x), o.x), __fadd_rn(__fmul_rn(n.w, d.y), o.y),
                     __fadd_rn(__fmul_rn(n.w, d.z), o.z), 0.f);
   } else if (lvl_rec) {
@@ -402,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   __shared__ int sh_ctrl[GROUPS];
   __shared__ float sh_pose32[GROUPS][12];
   __shared__ float4 sh_lvl[GROUPS][2];  // RK_ICP_LVL_SMEM: {gate2, 1/k, 1/s, stride}, {level off, level w}
+  __shared__ const float4* sh_surf[GROUPS];  // RK_ICP_LVL_SMEM: this pair's surfel base
   if (gtid < 12) sh_pose[g][gtid] = A.init12[pair * 12 + gtid];
   int n_done = 0, status = RK_ICP_CONVERGED;
 #if RK_ICP_TIME_SOLVE
@@ -436,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     if (RK_ICP_LVL_SMEM && gtid == 0) {
       sh_lvl[g][0] = make_float4(gate2, inv_k, inv_s, __int_as_float(stride));
       sh_lvl[g][1] = make_float4(__int_as_float(lvl_off), __int_as_float(lvl_w), 0.f, 0.f);
+      sh_surf[g] = surf;
     }
     // executed work (the roofline's unit) = valid points of this level x the
     // iterations run; counted once per level, outside the hot loop
@@ -493,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
             move_f32(P, r, d4, o4, mx, my, mz);
             if (RK_ICP_LVL_SMEM) {
               const float4 L0 = sh_lvl[g][0], L1 = sh_lvl[g][1];
-              associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, __float_as_int(L0.w),
+              associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, sh_surf[g], rec, __float_as_int(L0.w),
                                                  __float_as_int(L1.x), __float_as_int(L1.y), L0.z, L0.x,
                                                  L0.y, acc, cost, sumsq, cnt);
             } else {
