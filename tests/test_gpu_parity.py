@@ -757,3 +757,34 @@ def test_nvtx_tracing_is_transparent(rk, sensors, golden_icp):
     finally:
         trace.enable(False)
     assert np.array_equal(a.pose.matrix(), b.pose.matrix())
+
+
+def test_grid_pool_growth_is_transparent(rk, sensors, golden_tsdf, golden_icp):
+    """A pool far too small for the data (capacity 4 blocks) grows on
+    overflow and re-runs the activation: the per-call API leaves exactly the
+    grid and counts of a pre-sized pool (activate_blocks and
+    integrate_cloud_frame, sdf_volume.py:82-113, 198-210).  The batched
+    sequence path reports the overflow instead (caller-sized pool)."""
+    import torch
+    from paper_2112_02779_b200 import pipeline
+    small = rk.VoxelBlockGrid(voxel_size=0.1, capacity=4)
+    keys = rk.activate_blocks(golden_tsdf["act_pts"], small, 0.55)
+    assert sorted(keys) == [tuple(k) for k in golden_tsdf["act_keys"].tolist()]
+    assert small.info()[1] > 4 and not small.info()[2]
+    intr = sensors["ouster"]
+    frame = golden_icp["street/dst"]
+    pose = rk.RigidTransform.identity()
+    a = rk.VoxelBlockGrid(voxel_size=0.05, capacity=4)
+    b = rk.VoxelBlockGrid(voxel_size=0.05, capacity=16384)
+    for _ in range(2):
+        na = rk.integrate_cloud_frame(a, rk.RangeImage(frame, intr), pose, clip_max=30.0)
+        nb = rk.integrate_cloud_frame(b, rk.RangeImage(frame, intr), pose, clip_max=30.0)
+        assert na == nb
+    ka, va = a.export_blocks()
+    kb, vb = b.export_blocks()
+    assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+    c = rk.VoxelBlockGrid(voxel_size=0.05, capacity=4)
+    dev = torch.from_numpy(frame).cuda()[None]
+    rows = torch.from_numpy(pipeline.poses_to_rows([pose])).cuda()
+    pipeline.integrate_sequence(c, intr, dev, rows)
+    assert c.info()[2] == 1            # overflow flagged, never silent
