@@ -438,22 +438,37 @@ def _cpu_icp_job(seed_pairs):
     return len(imgs), time.perf_counter() - t0
 
 
-def cpu_icp_baseline(budget_s: float):
+def cpu_icp_baseline(budget_s: float, steps: int = 1, warmup: int = 0):
+    """The reference's CPU path (oracle port) on every host core: a process
+    pool of single-threaded workers, each registering its own pool pairs.
+    ``warmup`` untimed steps (one pair per worker), then ``steps`` timed
+    steps sized so the timed work totals about ``budget_s`` seconds; a
+    step's time is its slowest worker's compute time (rendering excluded)."""
     from concurrent.futures import ProcessPoolExecutor
     cores = os.cpu_count() or 1
+    steps = max(1, steps)
     # calibrate: one pair on one core
     n1, t1 = _cpu_icp_job([0])
-    per_worker = max(1, int(budget_s / max(t1, 1e-3) / 2))
-    jobs = [list(range(k * per_worker, (k + 1) * per_worker)) for k in range(cores)]
+    per_worker = max(1, int(budget_s / steps / max(t1, 1e-3) / 2))
+    done, busy, step_s = 0, 0.0, []
     t0 = time.perf_counter()
     with ProcessPoolExecutor(cores) as ex:
-        outs = list(ex.map(_cpu_icp_job, jobs))
+        for _ in range(warmup):
+            list(ex.map(_cpu_icp_job, [[k] for k in range(cores)]))
+        nxt = 0
+        for _ in range(steps):
+            jobs = [list(range(nxt + k * per_worker, nxt + (k + 1) * per_worker)) for k in range(cores)]
+            nxt += cores * per_worker
+            outs = list(ex.map(_cpu_icp_job, jobs))
+            done += sum(n for n, _ in outs)
+            step_s.append(max(t for _, t in outs))
     wall = time.perf_counter() - t0
-    done = sum(n for n, _ in outs)
-    busy = max(t for _, t in outs)
+    busy = sum(step_s)
     return dict(value=done / busy, unit="registrations/s", cores=cores, kind="port",
-                sample=f"{done} C4 pool pairs (normals + 3-level register), oracle numpy, "
-                       f"{cores} processes x 1 thread, {busy:.1f} s compute ({wall:.1f} s wall)")
+                ms_per_step=1e3 * busy / steps,
+                sample=f"{done} C4 pool pairs over {steps} step(s) after {warmup} warm-up step(s) "
+                       f"(normals + 3-level register), oracle numpy, {cores} processes x 1 thread, "
+                       f"{busy:.1f} s compute ({wall:.1f} s wall)")
 
 
 def cpu_tsdf_baseline(frames: int = 3):
@@ -528,13 +543,13 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
-        icp = cpu_icp_baseline(args.cpu_seconds)
+        icp = cpu_icp_baseline(args.cpu_seconds, args.steps, args.warmup)
         line = {"impl": "reference", "metric": METRIC, "value": icp["value"], "unit": "registrations/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * args.pairs / icp["value"], "higher_is_better": True,
+                "ms_per_step": icp["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-                "config": {"workload": "C4 65,536 64x1024 street pairs (bounded CPU sample) + C2 TSDF 5 cm",
-                           "pairs": args.pairs},
+                "config": {"workload": "C4 65,536 64x1024 street pairs (bounded CPU sample per step) "
+                                       "+ C2 TSDF 5 cm", "pairs": args.pairs},
                 "cpu_baseline": icp, "tsdf": cpu_tsdf_baseline(),
                 "e2e": {"value": icp["value"], "unit": "registrations/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
