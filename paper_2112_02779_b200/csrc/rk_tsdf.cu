@@ -280,6 +280,9 @@ __global__ void __launch_bounds__(kAssignThreads) k_assign_slots(GridDev g) {
 #ifndef RK_TSDF_FAST_PROJ
 #define RK_TSDF_FAST_PROJ 1
 #endif
+#ifndef RK_TSDF_STATIC
+#define RK_TSDF_STATIC 1
+#endif
 #ifndef RK_TSDF_EARLY_STATE
 #define RK_TSDF_EARLY_STATE 1
 #endif
@@ -339,6 +342,23 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
       A.global_touch ? (unsigned long long)A.global_touch[1] : A.g.tc->max_touched_key;
   const bool lone_tail = (n_all % kChunkBlocks) == 1;
   int count = 0;
+#if RK_TSDF_STATIC
+  // static round-robin blocks: the next block is known, so its metadata
+  // (touched entry -> slot, key) is loaded while the current one runs
+  int h_n = blockIdx.x < n_touched ? A.g.touched[blockIdx.x] : 0;
+  int slot_n = blockIdx.x < n_touched ? A.g.h_slot[h_n] : -1;
+  unsigned long long key_n = blockIdx.x < n_touched ? A.g.h_keys[h_n] : 0ull;
+  for (int e = blockIdx.x; e < n_touched; e += gridDim.x) {
+    const int slot = slot_n;
+    const unsigned long long key = key_n;
+    const int e2 = e + gridDim.x;
+    if (e2 < n_touched) {
+      h_n = A.g.touched[e2];
+      slot_n = A.g.h_slot[h_n];
+      key_n = A.g.h_keys[h_n];
+    }
+    if (slot < 0) continue;
+#else
   for (;;) {
     if (threadIdx.x == 0) sh_e = atomicAdd(&A.g.ctr->work, 1);
     __syncthreads();
@@ -349,6 +369,7 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
     const int slot = A.g.h_slot[h];
     if (slot < 0) continue;
     const unsigned long long key = A.g.h_keys[h];
+#endif
     int kx, ky, kz;
     unpack_key(key, kx, ky, kz);
     double base[3];
