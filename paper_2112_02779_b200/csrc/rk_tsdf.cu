@@ -311,7 +311,9 @@ template <int MATH, int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(IntegrateArgs A) {
   extern __shared__ float sh_off[];  // kVox*3 rotated lattice (48 KB, dynamic)
   __shared__ int sh_cnt[NT / 32];
+#if !RK_TSDF_STATIC
   __shared__ int sh_e;
+#endif
   __shared__ RowTablesSmem sh_tab;
   if (SMEM) stage_tables(A.s, sh_tab, threadIdx.x, NT);
   const RowTables tb = SMEM ? RowTables{sh_tab.el32, sh_tab.az32, sh_tab.inv_rows} : global_tables(A.s);
