@@ -62,6 +62,7 @@ constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
 #define RK_ICP_THREADS 256
 #endif
 constexpr int kThreads = RK_ICP_THREADS;  // one CTA per pair by default (WPP = kThreads / 32)
+constexpr int kWide = 1024;               // latency-mode CTA (small batches)
 
 struct IcpArgs {
   SensorDev s;
@@ -377,11 +378,11 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
   accumulate_point<STATS, FUSED>(mx, my, mz, n, q, gate2, inv_k, acc, cost, sumsq, cnt);
 }
 
-template <int WPP>
+template <int WPP, int NT>
 __device__ __forceinline__ void group_sync(int g) {
   if (WPP == 1) {
     __syncwarp();
-  } else if (WPP * 32 == kThreads) {
+  } else if (WPP * 32 == NT) {
     __syncthreads();
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(WPP * 32) : "memory");
@@ -390,9 +391,9 @@ __device__ __forceinline__ void group_sync(int g) {
 
 // STATS: accumulate the robust cost and squared residuals (IterationStats
 // rows); the pose update needs neither, so batch runs without stats skip them.
-template <int MATH, int WPP, int MINB, bool SMEM, bool STATS>
-__global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
-  constexpr int NW = kThreads / 32, GROUPS = NW / WPP, GT = WPP * 32;
+template <int MATH, int WPP, int MINB, bool SMEM, bool STATS, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
+  constexpr int NW = NT / 32, GROUPS = NW / WPP, GT = WPP * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp / WPP;
   const int gtid = tid - g * GT;
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
   const SensorDev& s = A.s;
   __shared__ RowTablesSmem sh_tab;
   if (SMEM) {
-    stage_tables(s, sh_tab, tid, kThreads);
+    stage_tables(s, sh_tab, tid, NT);
     __syncthreads();
   }
   if (pair >= A.batch) return;  // whole groups only (no CTA-wide barrier when GROUPS > 1)
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
     int executed = 0;
     for (int it = 0; it < A.cfg.iters[lv]; ++it) {
       ++executed;
-      group_sync<WPP>(g);  // pose (and sh_ctrl reuse) ready
+      group_sync<WPP, NT>(g);  // pose (and sh_ctrl reuse) ready
       // the pose is read from shared memory at every use (broadcast LDS):
       // holding it in registers would cost 24 of the registers the occupancy allows
       const double* pose = sh_pose[g];
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
       const float* P = sh_pose32[g];
       if (F32X) {
         if (gtid < 12) sh_pose32[g][gtid] = (float)pose[gtid];
-        group_sync<WPP>(g);
+        group_sync<WPP, NT>(g);
       }
       if (F32X && col_mode) {
         for (int cj = gtid; cj < Ws; cj += GT) {
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           sh_red[warp][28] = q2;
           sh_cnt[warp] = nc;
         }
-        group_sync<WPP>(g);
+        group_sync<WPP, NT>(g);
         if (gtid < kNumAcc) {
           double t = 0.0;
           for (int w2 = 0; w2 < WPP; ++w2) t += sh_red[g * WPP + w2][gtid];
@@ -631,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
         if (gtid == 0)
           for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
       }
-      group_sync<WPP>(g);
+      group_sync<WPP, NT>(g);
       if (gtid < 32) {  // the group's first warp updates the pose
         const int n_corr = sh_cnt[g * WPP];
         // (cfg fields by value: taking a kernel parameter's address would
@@ -665,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_register(IcpArgs A) {
           sh_ctrl[g] = ctrl;
         }
       }
-      group_sync<WPP>(g);
+      group_sync<WPP, NT>(g);
       const int ctrl = sh_ctrl[g];
       if (ctrl == 2) {
         work += valid_lv * executed;
@@ -685,7 +686,7 @@ finish:
     const unsigned w = __reduce_add_sync(0xffffffffu, work);
     if (lane == 0 && w) atomicAdd(A.pt_iters, (unsigned long long)w);
   }
-  group_sync<WPP>(g);
+  group_sync<WPP, NT>(g);
   if (gtid < 12) A.out12[pair * 12 + gtid] = sh_pose[g][gtid];
   if (gtid == 0) {
     A.status[pair] = status;
@@ -693,24 +694,37 @@ finish:
   }
 }
 
-template <int MATH, int WPP, int MINB>
+template <int MATH, int WPP, int MINB, int NT = kThreads>
 int launch(const IcpArgs& a, cudaStream_t st) {
-  constexpr int GROUPS = kThreads / 32 / WPP;
+  constexpr int GROUPS = NT / 32 / WPP;
   const unsigned grid = (unsigned)((a.batch + GROUPS - 1) / GROUPS);
   const bool smem = a.s.H <= kMaxRowsSmem && a.s.K <= kMaxInvSmem;
   if (a.stats) {
     if (smem)
-      k_register<MATH, WPP, MINB, true, true><<<grid, kThreads, 0, st>>>(a);
+      k_register<MATH, WPP, MINB, true, true, NT><<<grid, NT, 0, st>>>(a);
     else
-      k_register<MATH, WPP, MINB, false, true><<<grid, kThreads, 0, st>>>(a);
+      k_register<MATH, WPP, MINB, false, true, NT><<<grid, NT, 0, st>>>(a);
   } else {
     if (smem)
-      k_register<MATH, WPP, MINB, true, false><<<grid, kThreads, 0, st>>>(a);
+      k_register<MATH, WPP, MINB, true, false, NT><<<grid, NT, 0, st>>>(a);
     else
-      k_register<MATH, WPP, MINB, false, false><<<grid, kThreads, 0, st>>>(a);
+      k_register<MATH, WPP, MINB, false, false, NT><<<grid, NT, 0, st>>>(a);
   }
   RK_LAUNCHED("k_register");
   return RK_OK;
+}
+
+// SMs of the current device (cached per device)
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
 }
 
 }  // namespace
@@ -759,6 +773,12 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   constexpr int WFULL = kThreads / 32;
   if (cfg->math == MATH_CR)
     return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, WFULL, MINB>(a, st);
+  // latency mode: a batch that cannot fill the GPU with 256-thread CTAs
+  // (online odometry, one register() call, a short sequence) runs each pair
+  // on a 1024-thread CTA -- 4x the warps per pair to hide the gather latency
+  const char* wide = getenv("RK_ICP_WIDE");
+  if (!force && (!wide || atoi(wide)) && batch <= sm_count())
+    return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
   switch (wpp) {
     case 1: return launch<MATH_FAST, 1, MINB>(a, st);
     case 2: return launch<MATH_FAST, 2, MINB>(a, st);
