@@ -775,10 +775,13 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
     return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, WFULL, MINB>(a, st);
   // latency mode: a batch that cannot fill the GPU with 256-thread CTAs
   // (online odometry, one register() call, a short sequence) runs each pair
-  // on a 1024-thread CTA -- 4x the warps per pair to hide the gather latency
+  // on a 1024-thread CTA (<= one pair per SM) or a 512-thread CTA (<= two):
+  // more warps per pair to hide the gather latency
   const char* wide = getenv("RK_ICP_WIDE");
-  if (!force && (!wide || atoi(wide)) && batch <= sm_count())
-    return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
+  if (!force && (!wide || atoi(wide))) {
+    if (batch <= sm_count()) return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
+    if (batch <= 2 * sm_count()) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
+  }
   switch (wpp) {
     case 1: return launch<MATH_FAST, 1, MINB>(a, st);
     case 2: return launch<MATH_FAST, 2, MINB>(a, st);
