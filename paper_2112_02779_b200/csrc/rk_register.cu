@@ -778,6 +778,12 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   // on a 1024-thread CTA (<= one pair per SM) or a 512-thread CTA (<= two):
   // more warps per pair to hide the gather latency
   const char* wide = getenv("RK_ICP_WIDE");
+  const char* fnt = getenv("RK_ICP_NT");  // experiment knob: force the CTA size
+  if (!force && fnt) {
+    const int nt = atoi(fnt);
+    if (nt == 1024) return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
+    if (nt == 512) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
+  }
   if (!force && (!wide || atoi(wide))) {
     if (batch <= sm_count()) return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
     if (batch <= 2 * sm_count()) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
