@@ -45,7 +45,7 @@ enum {
 enum { RK_MATH_FAST = 0, RK_MATH_CR = 1, RK_MATH_LIBM = 2 };
 
 /* per-pair ICP status (registration.py:266-272) */
-enum { RK_ICP_CONVERGED = 0, RK_ICP_TOO_FEW = 1, RK_ICP_DEGENERATE = 2 };
+enum { RK_ICP_CONVERGED = 0, RK_ICP_TOO_FEW = 1, RK_ICP_DEGENERATE = 2, RK_ICP_BAD_PAIR = 3 };
 
 typedef struct rk_sensor rk_sensor; /* device-resident sensor tables   */
 typedef struct rk_grid rk_grid;     /* device voxel-block hash + pool  */
@@ -53,6 +53,9 @@ typedef struct rk_grid rk_grid;     /* device voxel-block hash + pool  */
 /* ------------------------------------------------------------ misc */
 int rk_last_error(char* buf_host, size_t cap);
 int rk_version(void);
+/* sizeof the ABI structs (0: rk_sensor_desc, 1: rk_icp_config; -1 otherwise):
+ * a binding checks its struct mirrors against these at load time */
+int rk_struct_size(int which);
 
 /* ------------------------------------------------------------ sensor
  * Replaces LidarIntrinsics' cached tables (lidar_model.py:94-179): the host
@@ -157,6 +160,10 @@ typedef struct {
    * its decimated map (< 0: use the full-resolution map at offset 0). */
   int64_t surfel_pitch;
   int32_t surfel_level_off[8];
+  /* image-pool sizes: a pair whose pair_src / pair_dst index lies outside
+   * [0, n) is not registered and gets status RK_ICP_BAD_PAIR (out12 = its
+   * init pose); 0 = unchecked */
+  int32_t n_src_images, n_dst_images;
 } rk_icp_config;
 
 /* projective_correspondences(single=True)  registration.py:117-187 for one
@@ -179,7 +186,11 @@ int rk_make_surfel(const float* range, const float* normals, const uint8_t* vali
  * stats (may be NULL): (B, max_total_iters, 5) float64 rows
  * {stride, iteration, n_correspondences, cost, inlier_rmse}.
  * pt_iters (may be NULL): device counter += executed source-point-iterations
- * (the roofline work unit). */
+ * (the roofline work unit).  One launch; each pair runs on one
+ * CTA: 256 threads for throughput batches, 512 / 1024 threads when the batch
+ * has <= 2 / <= 1 pairs per SM (latency mode; RK_ICP_WIDE=0 disables it).
+ * Pair indices are checked on the device against cfg->n_src_images /
+ * n_dst_images (RK_ICP_BAD_PAIR). */
 int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
                       const float* dst_surfel, const int32_t* pair_src,
                       const int32_t* pair_dst, int32_t batch, const double* init12,

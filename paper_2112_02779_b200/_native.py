@@ -38,13 +38,15 @@ class IcpConfig(C.Structure):
                 ("trans_eps", _f64), ("clip_min", _f32), ("clip_max", _f32),
                 ("n_levels", _i32), ("strides", _i32 * 8), ("iters", _i32 * 8),
                 ("min_corr", _i32), ("scale_with_stride", _i32), ("math", _i32),
-                ("surfel_pitch", _i64), ("surfel_level_off", _i32 * 8)]
+                ("surfel_pitch", _i64), ("surfel_level_off", _i32 * 8),
+                ("n_src_images", _i32), ("n_dst_images", _i32)]
 
 
 # name -> argtypes (restype is always int status)
 SIGNATURES = {
     "rk_last_error": [C.c_char_p, C.c_size_t],
     "rk_version": [],
+    "rk_struct_size": [C.c_int],
     "rk_sensor_create": [C.POINTER(SensorDesc), C.POINTER(_p)],
     "rk_sensor_destroy": [_p],
     "rk_project_f32": [_p, _p, _i64, C.c_int, _p, _p, _p, _p, _p],
@@ -115,6 +117,10 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    for which, st in ((0, SensorDesc), (1, IcpConfig)):
+        if lib.rk_struct_size(which) != C.sizeof(st):
+            raise DeviceError(f"{p.name}: {st.__name__} is {C.sizeof(st)} bytes here, "
+                              f"{lib.rk_struct_size(which)} in the library (stale build?)")
     if path is None:
         _lib = lib
     return lib

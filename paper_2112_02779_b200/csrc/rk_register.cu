@@ -408,12 +408,23 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
   const RowTables tb = SMEM ? RowTables{sh_tab.el32, sh_tab.az32, sh_tab.inv_rows} : global_tables(s);
   const int H = s.H, W = s.W;
   const size_t HW = (size_t)H * W;
-  const float* src = A.src_range + (size_t)A.pair_src[pair] * HW;
+  const int ps = A.pair_src[pair], pd = A.pair_dst[pair];
+  if ((A.cfg.n_src_images > 0 && (unsigned)ps >= (unsigned)A.cfg.n_src_images) ||
+      (A.cfg.n_dst_images > 0 && (unsigned)pd >= (unsigned)A.cfg.n_dst_images)) {
+    // an index outside the pools: no reads, a defined result (group-uniform exit)
+    if (gtid < 12) A.out12[pair * 12 + gtid] = A.init12[pair * 12 + gtid];
+    if (gtid == 0) {
+      A.status[pair] = RK_ICP_BAD_PAIR;
+      A.n_iters[pair] = 0;
+    }
+    return;
+  }
+  const float* src = A.src_range + (size_t)ps * HW;
   // a surfel pyramid (surfel_pitch != 0) holds RK_SURFEL_REC-byte records {n, range}(, {target});
   // {target}; a plain surfel map 16-byte {n, range}
   const bool rec = A.cfg.surfel_pitch != 0;
   const long long surf_pitch = rec ? (RK_SURFEL_REC / 16) * A.cfg.surfel_pitch : (long long)HW;
-  const float4* surf = A.dst_surfel + (size_t)A.pair_dst[pair] * surf_pitch;
+  const float4* surf = A.dst_surfel + (size_t)pd * surf_pitch;
 
   __shared__ double sh_pose[GROUPS][12];
   __shared__ double sh_red[NW][kNumAcc];

@@ -33,6 +33,9 @@ extern "C" int rk_last_error(char* buf, size_t cap) {
 }
 
 extern "C" int rk_version(void) { return 1; }
+extern "C" int rk_struct_size(int which) {
+  return which == 0 ? (int)sizeof(rk_sensor_desc) : which == 1 ? (int)sizeof(rk_icp_config) : -1;
+}
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }

@@ -27,7 +27,7 @@ from .se3 import RigidTransform
 DEFAULT_SCHEDULE = ((4, 20), (2, 20), (1, 10))
 SINGLE_SCALE_SCHEDULE = ((1, 50),)
 
-ICP_CONVERGED, ICP_TOO_FEW, ICP_DEGENERATE = 0, 1, 2
+ICP_CONVERGED, ICP_TOO_FEW, ICP_DEGENERATE, ICP_BAD_PAIR = 0, 1, 2, 3
 
 
 @dataclass(frozen=True)
@@ -262,6 +262,8 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     (coarse levels gather from compact decimated maps; computed if None);
     inits: (B, 12) float64 initial poses (default identity);
     pt_iters: optional (1,) int64 device counter of executed point-iterations.
+    Pair indices outside the pools are checked on the device: such pairs get
+    status ICP_BAD_PAIR and their init pose.
     """
     t = nat.torch()
     src = src_ranges.contiguous()
@@ -283,6 +285,7 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     max_it = config.max_iterations
     stats = t.empty((B, max_it, 5), dtype=t.float64, device=dev) if with_stats else None
     cfg = config.to_c(math)
+    cfg.n_src_images, cfg.n_dst_images = int(src.shape[0]), int(dst.shape[0])
     surf = dst_surfels
     if isinstance(dst_surfels, SurfelPyramid):
         missing = [s for s, _ in config.schedule if int(s) not in dst_surfels.offsets]

@@ -36,6 +36,10 @@ def test_load_and_version():
     lib = _native.load()
     assert lib.rk_version() == 1
     assert _native.last_error() == ""
+    # the ctypes mirrors of the ABI structs match the library's layout
+    import ctypes
+    assert lib.rk_struct_size(0) == ctypes.sizeof(_native.SensorDesc)
+    assert lib.rk_struct_size(1) == ctypes.sizeof(_native.IcpConfig)
 
 
 def test_sm100a_sass_present():

@@ -788,3 +788,24 @@ def test_grid_pool_growth_is_transparent(rk, sensors, golden_tsdf, golden_icp):
     rows = torch.from_numpy(pipeline.poses_to_rows([pose])).cuda()
     pipeline.integrate_sequence(c, intr, dev, rows)
     assert c.info()[2] == 1            # overflow flagged, never silent
+
+
+def test_register_batch_bad_pair_index(rk, sensors, golden_icp):
+    """Pair indices outside the image pools are caught on the device: the
+    pair gets ICP_BAD_PAIR and its init pose, no out-of-bounds read, and the
+    other pairs of the batch are unaffected."""
+    import torch
+    from paper_2112_02779_b200.registration import ICP_BAD_PAIR
+    intr = sensors["ouster"]
+    src = torch.from_numpy(golden_icp["street/src"]).cuda()[None].repeat(2, 1, 1)
+    dst = torch.from_numpy(golden_icp["street/dst"]).cuda()[None].repeat(2, 1, 1)
+    ok = rk.register_batch(intr, src, dst)
+    ps = torch.tensor([0, 5, 1, -1], dtype=torch.int32, device="cuda")
+    pd = torch.tensor([0, 1, 7, 1], dtype=torch.int32, device="cuda")
+    res = rk.register_batch(intr, src, dst, pair_src=ps, pair_dst=pd)
+    st = res.status.cpu().numpy()
+    assert list(st[1:]) == [ICP_BAD_PAIR] * 3 and st[0] == int(ok.status[0].item())
+    assert torch.equal(res.poses[0], ok.poses[0])
+    eye = torch.tensor([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0], dtype=torch.float64, device="cuda")
+    assert all(torch.equal(res.poses[i], eye) for i in (1, 2, 3))
+    assert res.iterations[1:].abs().sum().item() == 0
