@@ -7,6 +7,9 @@ cli.py:267-283 integrate) expressed as a few launches over device buffers.
   sequence as ONE register_batch launch + the host pose prefix product
 * ``odometry_integrate`` -- C2 end to end: odometry, then the sequence
   integrated at the estimated poses
+* ``eval_registration`` -- cli.py:294-328 ``cmd_eval_reg``: every sampled
+  (i, i+d) pair of a sequence registered in ONE batched launch, scored
+  against the ground-truth relative poses (the registration CSV rows)
 * ``integrate_sequence`` -- activate + integrate F posed frames into one grid
   with no host synchronisation between frames
 * ``shard`` / ``gather_poses`` -- one-process-per-GPU partitioning of
@@ -178,6 +181,98 @@ def odometry_integrate(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames,
     updated = integrate_sequence(grid, intr, frames, poses_w, inv_w, clip_min=clip_min,
                                  clip_max=clip_max, graph=graph)
     return world, res, updated
+
+
+REGISTRATION_CSV_HEADER = ("frame_distance,pair_index,rot_err_rad,trans_err_m,"
+                           "converged,iters,runtime_ms")   # io_formats.py:368-369
+
+
+def rotation_error(R, R_gt) -> float:
+    """Geodesic angle arccos((trace(R R_gt^T) - 1) / 2) (eval_metrics.py:16-21)."""
+    c = (np.trace(np.asarray(R, float) @ np.asarray(R_gt, float).T) - 1.0) / 2.0
+    return float(np.arccos(np.clip(c, -1.0, 1.0)))
+
+
+def translation_error(t, t_gt) -> float:
+    """||t - t_gt|| in metres (eval_metrics.py:24-26)."""
+    return float(np.linalg.norm(np.asarray(t, float) - np.asarray(t_gt, float)))
+
+
+def sample_pairs(n_frames: int, frame_distance: int, count: int, seed=None):
+    """count seeded (i, i + d) pairs without replacement when possible
+    (eval_metrics.py:57-70, same generator calls, so the same pairs)."""
+    from .errors import EmptyInput
+    if frame_distance < 1:
+        raise ValueError("frame distance must be >= 1")
+    n_valid = n_frames - frame_distance
+    if n_valid < 1:
+        raise EmptyInput(f"no frame pairs at distance {frame_distance} in {n_frames} frames")
+    if count >= n_valid:
+        starts = np.arange(n_valid)
+    else:
+        starts = np.sort(np.random.default_rng(seed).choice(n_valid, size=count, replace=False))
+    return [(int(i), int(i + frame_distance)) for i in starts]
+
+
+@nvtx("eval_registration")
+def eval_registration(intr: lm.LidarIntrinsics, frames, gt_poses, distances, pairs: int,
+                      seed: int = 0, config: RegistrationConfig = RegistrationConfig(),
+                      init: str = "identity"):
+    """``cmd_eval_reg`` (cli.py:294-328) over a (F, H, W) device sequence:
+    for each frame distance d, ``sample_pairs(F, d, pairs, seed + d)``; pair
+    (i, j) registers frame j to frame i (init identity or centroid) and is
+    scored against gt[i]^-1 @ gt[j].  All pairs of all distances run as ONE
+    register_batch launch over one surfel pyramid of the sequence (the
+    reference runs them on a thread pool, one register() each).
+
+    Returns the CSV rows (d, pair_index, rot_err_rad, trans_err_m, converged,
+    iters, runtime_ms); runtime_ms is the batch's wall time divided by the
+    number of pairs (the amortised per-pair cost of the batched launch)."""
+    import time
+    t = nat.torch()
+    F = int(frames.shape[0])
+    jobs = []
+    for d in distances:
+        for k, (i, j) in enumerate(sample_pairs(F, int(d), pairs, seed=seed + int(d))):
+            jobs.append((int(d), k, i, j))
+    if not jobs:
+        return []
+    frames = frames.contiguous()
+    dev = nat.device()
+    t.cuda.synchronize()
+    t0 = time.perf_counter()
+    pair_dst = t.tensor([i for _, _, i, _ in jobs], dtype=t.int32, device=dev)
+    pair_src = t.tensor([j for _, _, _, j in jobs], dtype=t.int32, device=dev)
+    inits = None
+    if init == "centroid":
+        clouds = {}
+        for f in {x for _, _, i, j in jobs for x in (i, j)}:
+            clouds[f] = to_point_cloud(RangeImage(frames[f], intr))
+        inits = nat.to_dev(np.stack([initial_translation_by_centroids(clouds[j], clouds[i]).as_row12()
+                                     for _, _, i, j in jobs]), np.float64)
+    elif init != "identity":
+        raise ValueError("init must be 'identity' or 'centroid'")
+    surf = normals_cross_batch(intr, frames, strides=[s for s, _ in config.schedule])
+    res = register_batch(intr, frames, frames, surf, pair_src, pair_dst, inits, config)
+    poses = nat.to_host(res.poses)
+    status = nat.to_host(res.status)
+    iters = nat.to_host(res.iterations)
+    ms = 1e3 * (time.perf_counter() - t0) / len(jobs)
+    rows = []
+    for b, (d, k, i, j) in enumerate(jobs):
+        rel_gt = gt_poses[i].inverse() @ gt_poses[j]
+        R, tt = poses[b, :9].reshape(3, 3), poses[b, 9:]
+        rows.append((d, k, rotation_error(R, rel_gt.R), translation_error(tt, rel_gt.t),
+                     int(status[b] == 0), int(iters[b]), round(ms, 3)))
+    return rows
+
+
+def write_registration_csv(path, rows) -> None:
+    """io_formats.py:373-378."""
+    with open(path, "w", encoding="utf-8") as f:
+        f.write(REGISTRATION_CSV_HEADER + "\n")
+        for r in rows:
+            f.write(",".join(str(x) for x in r) + "\n")
 
 
 # launches issued per call (the bench's gpu_launches accounting)

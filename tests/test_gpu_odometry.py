@@ -110,3 +110,27 @@ def test_noisy_odometry_same_outcome():
         p = res.pose(k)
         assert np.all(np.isfinite(p.R)) and np.all(np.isfinite(p.t))
         assert (np.abs(p.t - gt.t).max() < 0.05) == (np.abs(ref["t"] - gt.t).max() < 0.05), k
+
+
+def test_eval_registration_rows_match_oracle(seq):
+    """cmd_eval_reg (cli.py:294-328) as one batched launch: the sampled
+    pairs, and per pair the rotation / translation errors against the ground
+    truth (eval_metrics.py:16-26) within the pose tolerance, the same
+    iteration count and convergence flag as the oracle's register()."""
+    import torch
+    from oracle import icp as oicp
+    from oracle import image as oimg
+    from paper_2112_02779_b200 import pipeline
+    intr, S, traj, frames = seq
+    rows = pipeline.eval_registration(intr, torch.from_numpy(frames).cuda(), traj, distances=[1, 2],
+                                      pairs=3, seed=0)
+    jobs = [(d, k, i, j) for d in (1, 2)
+            for k, (i, j) in enumerate(pipeline.sample_pairs(N_FRAMES, d, 3, seed=d))]
+    assert [(r[0], r[1]) for r in rows] == [(d, k) for d, k, _, _ in jobs]
+    for r, (d, k, i, j) in zip(rows, jobs):
+        vec, valid = oimg.normals_cross(S, frames[i])
+        ref = oicp.register(S, frames[j], frames[i], vec, valid)
+        rel = traj[i].inverse() @ traj[j]
+        assert abs(r[2] - pipeline.rotation_error(ref["R"], rel.R)) < 2e-5
+        assert abs(r[3] - pipeline.translation_error(ref["t"], rel.t)) < 2e-5
+        assert r[4] == int(ref["converged"]) and r[5] == len(ref["stats"])

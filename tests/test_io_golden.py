@@ -77,3 +77,18 @@ def test_intrinsics_json_cases_match_reference(gold, tmp_path):
             assert np.array_equal(np.asarray(v.ray_dirs), gold[f"json/{name}/ray_dirs"]), name
             assert np.array_equal(np.asarray(v.ray_origins), gold[f"json/{name}/ray_origins"]), name
             assert np.array_equal(np.asarray(v.fov_bounds, dtype=np.float64), gold[f"json/{name}/fov"]), name
+
+
+def test_sample_pairs_matches_reference():
+    """eval_metrics.sample_pairs (eval_metrics.py:57-70): the reference's
+    outputs, recorded with
+    PYTHONPATH=/root/reference/pkg/src python -c "from rangekit import eval_metrics as e;
+    print(e.sample_pairs(20, 3, 5, seed=4), e.sample_pairs(6, 2, 9, seed=1))"."""
+    from paper_2112_02779_b200 import pipeline
+    from paper_2112_02779_b200.errors import EmptyInput
+    assert pipeline.sample_pairs(20, 3, 5, seed=4) == [(8, 11), (9, 12), (13, 16), (14, 17), (15, 18)]
+    assert pipeline.sample_pairs(6, 2, 9, seed=1) == [(0, 2), (1, 3), (2, 4), (3, 5)]
+    with pytest.raises(EmptyInput):
+        pipeline.sample_pairs(3, 3, 1)
+    with pytest.raises(ValueError):
+        pipeline.sample_pairs(10, 0, 1)
