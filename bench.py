@@ -172,7 +172,7 @@ class TsdfRunner:
         rkd.broadcast_frames(frames, poses_w, src=0, dist=self.dist)
         self.dist.broadcast(inv_w, 0)
         return self.sharded.integrate_frames(self.intr, frames, poses_w, inv_w, clip_max=30.0,
-                                             updated=updated)
+                                             updated=updated, graph=True)
 
 
 def run_ours(args, rank, world, dist):
@@ -191,7 +191,6 @@ def run_ours(args, rank, world, dist):
     stream = torch.cuda.current_stream()
     pt_iters = torch.zeros(1, dtype=torch.int64, device=device)
     updated = torch.zeros(1, dtype=torch.int64, device=device)
-    updated_warm = torch.zeros(1, dtype=torch.int64, device=device)
 
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for k in ("normals", "icp", "tsdf")}
@@ -207,7 +206,9 @@ def run_ours(args, rank, world, dist):
                                 pair_dst=D["pair_dst"], config=cfg, pt_iters=pt_iters if timed else None)
         ev["icp"][1].record(stream)
         ev["tsdf"][0].record(stream)
-        tsdf.run(D["frames"], D["poses_w"], D["inv_w"], updated if timed else updated_warm)
+        # one counter for warm-up and timed steps: the TSDF CUDA graphs are keyed
+        # by their buffers, so all recording happens in the warm-up
+        tsdf.run(D["frames"], D["poses_w"], D["inv_w"], updated)
         ev["tsdf"][1].record(stream)
         return res
 
@@ -223,6 +224,7 @@ def run_ours(args, rank, world, dist):
     terr = np.linalg.norm(poses[:, 9:] - gts[:, 9:], axis=1)
     ok_frac = float(np.mean(terr < 0.05))
 
+    updated.zero_()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()

@@ -120,37 +120,82 @@ class ShardedGrid:
         from .sdf_volume import VoxelBlockGrid
         self.grid = VoxelBlockGrid(voxel_size=voxel_size, **grid_kw)
         self.rank, self.world, self.dist = rank, world, dist
+        self._slots = 0   # touched-set slots reserved so far (graphs live in grid._graphs)
         nat.call("rk_grid_set_shard", self.grid._ensure(), int(rank), int(world))
 
     def integrate_frames(self, intr, frames, poses_w, inv_w, clip_min=0.0, clip_max=np.inf,
-                         updated=None):
+                         updated=None, graph: bool = False, reduce=None):
         """integrate_cloud_frame for F frames on this rank's shard.  frames /
         poses must already be identical on every rank (see broadcast_frames).
 
         All F frames are activated first (one touched-set slot each), the
         per-frame {count, max key} pairs are reduced across ranks in one
         collective (the reference's sorted-chunk arithmetic needs the global
-        values), then the F integrations run back to back."""
+        values), then the F integrations run back to back.
+
+        graph=True records the two device phases (3F activation launches +
+        the stats export; F integrations) as two CUDA graphs on the first
+        call with these buffers and replays them afterwards, so a step costs
+        two graph launches and one collective instead of ~4F kernel launches
+        (at 8 ranks the per-rank GPU work of a 100-frame sequence is shorter
+        than issuing those launches).  ``reduce`` overrides the collective
+        (tests emulate several shards in one process)."""
         from . import lidar_model as lm
         g = self.grid
         h = g._prepare()
         sensor = lm.device_sensor(intr)
         if updated is None:
             updated = nat.zeros((1,), np.int64)
-        st = nat.stream_ptr()
         F = int(frames.shape[0])
         cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
         frames, poses_w, inv_w = frames.contiguous(), poses_w.contiguous(), inv_w.contiguous()
-        nat.call("rk_grid_reserve_slots", h, F, st)
-        nat.call("rk_grid_activate_frames", h, sensor, nat.ptr(frames), F, nat.ptr(poses_w),
-                 float(g.truncation), cmin, cmax, st)
-        glob = None
-        if self.world > 1:
-            stats = nat.zeros((F, 2), np.int64)
-            nat.call("rk_grid_touch_stats_frames", h, F, nat.ptr(stats), st)
-            glob = reduce_touch_stats_frames(stats, self.dist)
-        nat.call("rk_grid_integrate_activated", h, sensor, nat.ptr(frames), F, nat.ptr(inv_w),
-                 nat.ptr(glob), cmin, cmax, lm.default_math(), nat.ptr(updated), st)
+        sharded = self.world > 1 or reduce is not None
+        red = reduce or (lambda st: reduce_touch_stats_frames(st, self.dist))
+        if F > self._slots:
+            # growing the touched-set slots reallocates them: recorded graphs
+            # (this grid's, incl. integrate_sequence's) point at the old ones
+            g._graphs.clear()
+            self._slots = F
+        nat.call("rk_grid_reserve_slots", h, F, nat.stream_ptr())
+        key = ("sharded", sensor, frames.data_ptr(), F, poses_w.data_ptr(), inv_w.data_ptr(),
+               updated.data_ptr(), cmin, cmax, lm.default_math())
+        bufs = g._graphs.get(key) if graph else None
+        if bufs is None:
+            bufs = dict(stats=nat.zeros((F, 2), np.int64), glob=nat.zeros((F, 2), np.int64))
+
+        def activate():
+            st = nat.stream_ptr()
+            nat.call("rk_grid_activate_frames", h, sensor, nat.ptr(frames), F, nat.ptr(poses_w),
+                     float(g.truncation), cmin, cmax, st)
+            if sharded:
+                nat.call("rk_grid_touch_stats_frames", h, F, nat.ptr(bufs["stats"]), st)
+
+        def integrate():
+            nat.call("rk_grid_integrate_activated", h, sensor, nat.ptr(frames), F, nat.ptr(inv_w),
+                     nat.ptr(bufs["glob"]) if sharded else None, cmin, cmax, lm.default_math(),
+                     nat.ptr(updated), nat.stream_ptr())
+
+        if not graph:
+            activate()
+            if sharded:
+                bufs["glob"].copy_(red(bufs["stats"]))
+            integrate()
+        else:
+            if "ga" not in bufs:
+                torch = nat.torch()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                for name, fn in (("ga", activate), ("gi", integrate)):
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, stream=side):
+                        fn()
+                    bufs[name] = gr
+                torch.cuda.current_stream().wait_stream(side)
+                g._graphs[key] = bufs
+            bufs["ga"].replay()
+            if sharded:
+                bufs["glob"].copy_(red(bufs["stats"]))
+            bufs["gi"].replay()
         g.blocks._bump()
         return updated
 

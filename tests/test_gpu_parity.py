@@ -809,3 +809,52 @@ def test_register_batch_bad_pair_index(rk, sensors, golden_icp):
     eye = torch.tensor([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0], dtype=torch.float64, device="cuda")
     assert all(torch.equal(res.poses[i], eye) for i in (1, 2, 3))
     assert res.iterations[1:].abs().sum().item() == 0
+
+
+def test_sharded_frames_graph_replay_matches_eager(rk, sensors):
+    """ShardedGrid.integrate_frames(graph=True): the two recorded phases
+    (activation of all F frames + stats export; the F integrations) replayed
+    around the collective reproduce the eager flow bit for bit, for a lone
+    grid and for each of two emulated shards (the collective replaced by the
+    precomputed global {count, max key} pairs)."""
+    import torch
+    from paper_2112_02779_b200 import distributed as rkd
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = sensors["ouster"]
+    traj = scenes.street_trajectory(5, seed=0)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    poses = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    inv = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).cuda()
+    # lone grid (world 1): eager vs record + replay
+    lone = rkd.ShardedGrid(0.05, 0, 1, capacity=8192)
+    ref = None
+    for graph in (False, True, True):
+        pipeline.clear_grid(lone.grid)
+        upd = torch.zeros(1, dtype=torch.int64, device="cuda")
+        lone.integrate_frames(intr, frames, poses, inv, clip_max=30.0, updated=upd, graph=graph)
+        k, v = lone.grid.export_blocks()
+        if ref is None:
+            ref = (int(upd.item()), k, v)
+        else:
+            assert int(upd.item()) == ref[0] and np.array_equal(k, ref[1]) and np.array_equal(v, ref[2])
+    # two shards: global stats from an eager activation pass of both
+    shards = [rkd.ShardedGrid(0.05, r, 2, capacity=8192) for r in range(2)]
+    stats = []
+    for sh in shards:
+        sh.integrate_frames(intr, frames, poses, inv, clip_max=30.0,
+                            reduce=lambda st: stats.append(st.clone()) or st)
+    glob = torch.stack([stats[0][:, 0] + stats[1][:, 0], torch.maximum(stats[0][:, 1], stats[1][:, 1])],
+                       -1).contiguous()
+    for sh in shards:
+        outs = []
+        for graph in (False, True, True):
+            pipeline.clear_grid(sh.grid)
+            upd = torch.zeros(1, dtype=torch.int64, device="cuda")
+            sh.integrate_frames(intr, frames, poses, inv, clip_max=30.0, updated=upd, graph=graph,
+                                reduce=lambda st: glob)
+            outs.append((int(upd.item()),) + sh.grid.export_blocks())
+        for n, k, v in outs[1:]:
+            assert n == outs[0][0] and np.array_equal(k, outs[0][1]) and np.array_equal(v, outs[0][2])
+    # and the shards together equal the lone grid
+    k = np.concatenate([sh.grid.export_blocks()[0] for sh in shards])
+    assert len(k) == len(ref[1])
