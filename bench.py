@@ -42,7 +42,8 @@ TSDF_BYTES_PER_PIXEL = 4
 TSDF_VOXEL = {"c2": 0.05, "c3": 0.10, "c5": 0.03}
 TSDF_DESC = {"c2": "C2: {n}-frame 64x1024 street sequence, TSDF 5 cm",
              "c3": "C3: {n}-frame HDL-64 64x2048 street sequence, TSDF 10 cm",
-             "c5": "C5: {n}-frame OS-128 128x2048 street sequence, TSDF 3 cm"}
+             "c5": "C5: {n}-frame OS-128 128x2048 extended-street sequence (0.5 m/frame), TSDF 3 cm"}
+TSDF_CAPACITY = {"c2": 65536, "c3": 65536, "c5": 262144}   # voxel blocks (32 KB each)
 
 
 def parse():
@@ -132,8 +133,15 @@ def make_inputs(args, rank, world, device):
     idx = (np.arange(lo, hi, dtype=np.int64) * 1237) % args.pool
     pair_idx = torch.from_numpy(idx.astype(np.int32)).to(device)
     tintr = {"c2": intr, "c3": scenes.hdl64(), "c5": scenes.os128()}[args.tsdf_config]
-    traj = scenes.street_trajectory(args.frames, seed=0)
-    frames = pipeline.render_batch(tintr, street, traj)
+    if args.tsdf_config == "c5":
+        # C5: the extended street at 0.5 m/frame
+        # small twist jitter: over 1,000 frames the default +-2 mrad random walk
+        # takes the sensor below the ground slab (z drifts ~4 m)
+        traj = scenes.street_trajectory(args.frames, seed=0, step_m=0.5, jitter=0.0002)
+        frames = pipeline.render_batch(tintr, scenes.extended_street_scene(0.5 * args.frames + 30.0), traj)
+    else:
+        traj = scenes.street_trajectory(args.frames, seed=0)
+        frames = pipeline.render_batch(tintr, street, traj)
     poses_w = torch.from_numpy(pipeline.poses_to_rows(traj)).to(device)
     inv_w = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).to(device)
     gts = np.stack([gt.as_row12() for _, gt in pool])
@@ -150,16 +158,16 @@ class TsdfRunner:
     hash-sharded over the ranks (each integrates its own blocks for every
     frame) and rank 0 broadcasts the frames + poses over NCCL first."""
 
-    def __init__(self, intr, rank, world, dist, voxel=0.05):
+    def __init__(self, intr, rank, world, dist, voxel=0.05, capacity=65536):
         import paper_2112_02779_b200 as rk
         from paper_2112_02779_b200 import distributed as rkd
         self.intr, self.world, self.dist = intr, world, dist
         if world > 1:
-            self.sharded = rkd.ShardedGrid(voxel, rank, world, dist, capacity=65536)
+            self.sharded = rkd.ShardedGrid(voxel, rank, world, dist, capacity=capacity)
             self.grid = self.sharded.grid
         else:
             self.sharded = None
-            self.grid = rk.VoxelBlockGrid(voxel_size=voxel, capacity=65536)
+            self.grid = rk.VoxelBlockGrid(voxel_size=voxel, capacity=capacity)
 
     def run(self, frames, poses_w, inv_w, updated):
         from paper_2112_02779_b200 import distributed as rkd
@@ -186,7 +194,8 @@ def run_ours(args, rank, world, dist):
     D = make_inputs(args, rank, world, device)
     intr = D["intr"]
     cfg = rk.RegistrationConfig()
-    tsdf = TsdfRunner(D["tintr"], rank, world, dist, TSDF_VOXEL[args.tsdf_config])
+    tsdf = TsdfRunner(D["tintr"], rank, world, dist, TSDF_VOXEL[args.tsdf_config],
+                      TSDF_CAPACITY[args.tsdf_config])
     grid = tsdf.grid
     stream = torch.cuda.current_stream()
     pt_iters = torch.zeros(1, dtype=torch.int64, device=device)
@@ -316,7 +325,8 @@ def run_ours(args, rank, world, dist):
     odo = None
     if dist is None:
         traj = D["traj"]
-        og = rk.VoxelBlockGrid(voxel_size=TSDF_VOXEL[args.tsdf_config], capacity=65536)
+        og = rk.VoxelBlockGrid(voxel_size=TSDF_VOXEL[args.tsdf_config],
+                               capacity=TSDF_CAPACITY[args.tsdf_config])
         od_ms = []
         for _ in range(4):
             pipeline.clear_grid(og)

@@ -185,6 +185,10 @@ __device__ __forceinline__ int warp_solve_step(const double* tot, int n_corr, do
     for (int i = 0; i < 6; ++i) tr = __fma_rn(m[i], m[i], tr);
 #pragma unroll
   for (int off = 4; off > 0; off >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, off);
+  // the xor tree sums lanes 0-7 only: broadcast lane 0's total so the branch
+  // below is warp-uniform (lanes >= 8 held 0 and would skip the exact
+  // fallback while lanes 0-7 take it -- diverged full-mask shuffles, a hang)
+  tr = __shfl_sync(0xffffffffu, tr, 0);
   if (!(sqrt(fh) * tr <= 1e12)) {  // inside the bounds' band: exact eigenvalues decide
     int ctrl = 0;
     if (lane == 0) ctrl = solve_step(tot, n_corr, pose, min_corr, rot_eps, trans_eps, status);
@@ -644,6 +648,9 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
       }
       group_sync<WPP, NT>(g);
+#if RK_ICP_TRACE
+      if (gtid == 0) printf("pair %d lv %d it %d reduced n %d\n", pair, lv, it, sh_cnt[g * WPP]);
+#endif
       if (gtid < 32) {  // the group's first warp updates the pose
         const int n_corr = sh_cnt[g * WPP];
         // (cfg fields by value: taking a kernel parameter's address would
@@ -679,6 +686,10 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
       }
       group_sync<WPP, NT>(g);
       const int ctrl = sh_ctrl[g];
+#if RK_ICP_TRACE
+      if (gtid == 0) printf("pair %d lv %d it %d n %d ctrl %d t %.6f %.6f %.6f\n", pair, lv, it, sh_cnt[g * WPP], ctrl,
+                            sh_pose[g][9], sh_pose[g][10], sh_pose[g][11]);
+#endif
       if (ctrl == 2) {
         work += valid_lv * executed;
         goto finish;

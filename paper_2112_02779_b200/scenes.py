@@ -79,6 +79,25 @@ def street_scene():
             ("sphere", (-3.0, -6.0, -0.3), 1.5)]
 
 
+def extended_street_scene(length_m: float, y0: float = -14.0):
+    """C5's extended street: the street's two façades and ground
+    slab run ``length_m`` along +y from ``y0``, with a box and a sphere
+    repeated every 10 m (street_scene's kerb-side objects) and a cross wall
+    closing each end."""
+    L = float(length_m)
+    yc = y0 + 0.5 * L
+    prims = [("box", (8.0, yc, 2.0), (0.5, L, 8.0), None),
+             ("box", (-8.0, yc, 2.0), (0.5, L, 8.0), None),
+             ("box", (0.0, yc, -2.05), (17.0, L + 1.0, 0.5), None),
+             ("box", (0.0, y0, 2.0), (18.0, 0.5, 8.0), None),
+             ("box", (0.0, y0 + L, 2.0), (18.0, 0.5, 8.0), None)]
+    for k in range(int(L // 10.0)):
+        y = y0 + 10.0 * k
+        prims.append(("box", (4.0, y + 6.0, -1.0), (2.0, 3.0, 2.0), None))
+        prims.append(("sphere", (-3.0, y + 2.0, -0.3), 1.5))
+    return prims
+
+
 def room_scene():
     return [("box", (6.0, 0.0, 1.0), (0.4, 16.0, 6.0), None),
             ("box", (0.0, 7.0, 1.0), (16.0, 0.4, 6.0), None),

@@ -858,3 +858,24 @@ def test_sharded_frames_graph_replay_matches_eager(rk, sensors):
     # and the shards together equal the lone grid
     k = np.concatenate([sh.grid.export_blocks()[0] for sh in shards])
     assert len(k) == len(ref[1])
+
+
+@pytest.mark.timeout(300)
+def test_register_ill_conditioned_corridor_terminates(rk):
+    """Regression: a pair whose normal equations fall in the band between the
+    condition-number bounds (the sensor drifted below the ground slab of the
+    C5 extended street: a corridor of parallel planes) takes the exact serial
+    fallback; the warp-parallel update once let lanes 0-7 branch into it while
+    lanes 8-31 continued (a non-uniform trace bound), deadlocking the warp's
+    full-mask shuffles.  It must finish with a defined status."""
+    import torch
+    from paper_2112_02779_b200 import pipeline, scenes
+    from paper_2112_02779_b200.registration import ICP_BAD_PAIR
+    intr = scenes.os128()
+    traj = scenes.street_trajectory(438, seed=0, step_m=0.5)   # default 2 mrad jitter
+    frames = pipeline.render_batch(intr, scenes.extended_street_scene(330.0), traj[436:438])
+    res = rk.register_batch(intr, frames[1:2], frames[0:1])
+    torch.cuda.synchronize()
+    st = int(res.status[0].item())
+    assert st in (0, 1, 2) and st != ICP_BAD_PAIR
+    assert torch.isfinite(res.poses).all()
