@@ -879,3 +879,47 @@ def test_register_ill_conditioned_corridor_terminates(rk):
     st = int(res.status[0].item())
     assert st in (0, 1, 2) and st != ICP_BAD_PAIR
     assert torch.isfinite(res.poses).all()
+
+
+@pytest.mark.timeout(300)
+def test_register_batch_stress_terminates(rk):
+    """Termination and defined outputs on hostile inputs, one batch: large
+    perturbations (up to 25 deg / 4 m), 5-cm range noise, all-sky and empty
+    images, a sensor below the ground, and the C5 corridor pairs whose
+    normal equations are singular or in the condition bounds' band."""
+    import torch
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = scenes.ouster64()
+    street = scenes.street_scene()
+    g = np.random.default_rng(123)
+    dst_poses, src_poses = [], []
+    for k in range(96):
+        yaw = g.uniform(-np.pi, np.pi)
+        base = rk.RigidTransform.exp(np.array([0, 0, yaw, g.uniform(-4, 4), g.uniform(-9, 9),
+                                               g.uniform(-3.0, 0.5)]))
+        pert = scenes.perturbation_pose(np.random.default_rng(k), g.uniform(0, 25), g.uniform(0, 4))
+        dst_poses.append(base)
+        src_poses.append(base @ pert)
+    dst = pipeline.render_batch(intr, street, dst_poses)
+    src = pipeline.render_batch(intr, street, src_poses)
+    noise = torch.randn_like(src) * 0.05
+    src = torch.where(src > 0, (src + noise).clamp_min(0.0), src)
+    src[0] = 0.0                      # empty source
+    dst[1] = 0.0                      # empty destination
+    src[2, 20:] = 0.0                 # mostly sky
+    res = rk.register_batch(intr, src, dst)
+    torch.cuda.synchronize()
+    st = res.status.cpu().numpy()
+    assert set(np.unique(st)) <= {0, 1, 2}
+    assert torch.isfinite(res.poses).all()
+    assert st[0] == 1 and st[1] == 1
+    # the C5 corridor: a jittered 500-frame drive that leaves the street
+    c5 = scenes.os128()
+    traj = scenes.street_trajectory(600, seed=0, step_m=0.5)
+    frames = pipeline.render_batch(c5, scenes.extended_street_scene(330.0), traj[400:600])
+    ps = torch.arange(1, 200, dtype=torch.int32, device="cuda")
+    res = rk.register_batch(c5, frames, frames, pair_src=ps, pair_dst=ps - 1)
+    torch.cuda.synchronize()
+    st = res.status.cpu().numpy()
+    assert set(np.unique(st)) <= {0, 1, 2} and (st == 2).any()
+    assert torch.isfinite(res.poses).all()
