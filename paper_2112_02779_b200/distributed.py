@@ -187,7 +187,7 @@ class ShardedGrid:
                 side.wait_stream(torch.cuda.current_stream())
                 for name, fn in (("ga", activate), ("gi", integrate)):
                     gr = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(gr, stream=side):
+                    with torch.cuda.graph(gr, stream=side, capture_error_mode="thread_local"):
                         fn()
                     bufs[name] = gr
                 torch.cuda.current_stream().wait_stream(side)

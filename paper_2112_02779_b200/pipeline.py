@@ -119,7 +119,7 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
             g = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.graph(g, stream=side):
+            with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
                 issue()
             torch.cuda.current_stream().wait_stream(side)
             grid._graphs[key] = g
