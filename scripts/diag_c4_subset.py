@@ -1,3 +1,5 @@
+"""Per-pair diagnostic of the C4 256-pair parity subset: GPU (FAST, or CR=1)
+vs the oracle; prints the well-posed pairs outside 1e-5 / equal iterations."""
 import sys, os
 sys.path.insert(0, '.')
 sys.argv = ['x']
@@ -11,7 +13,9 @@ pool = scenes.pair_pool_poses(2048, seed=0)
 pick = np.random.default_rng(2026).choice(len(pool), size=256, replace=False)
 src = pipeline.render_batch(intr, street, [pool[i][0] @ pool[i][1] for i in pick])
 dst = pipeline.render_batch(intr, street, [pool[i][0] for i in pick])
-res = rk.register_batch(intr, src, dst, with_stats=True)
+from paper_2112_02779_b200 import lidar_model as lm
+MATH = lm.MATH_CR if os.environ.get('CR') else None
+res = rk.register_batch(intr, src, dst, with_stats=True, math=MATH)
 poses = res.poses.cpu().numpy(); iters = res.iterations.cpu().numpy()
 src_h, dst_h = src.cpu().numpy(), dst.cpu().numpy()
 gt = np.stack([pool[i][1].as_row12() for i in pick])
