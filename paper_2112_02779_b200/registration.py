@@ -268,6 +268,18 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     t = nat.torch()
     src = src_ranges.contiguous()
     dst = dst_ranges.contiguous()
+    hw = (intr.height, intr.width)
+    for name, x in (("src_ranges", src), ("dst_ranges", dst)):
+        if not (nat.is_tensor(x) and x.is_cuda and x.dtype == t.float32 and x.ndim == 3
+                and tuple(x.shape[1:]) == hw):
+            raise ValueError(f"{name} must be a (P, {hw[0]}, {hw[1]}) float32 CUDA tensor")
+    if isinstance(dst_surfels, SurfelPyramid):
+        if dst_surfels.data.shape[0] != dst.shape[0]:
+            raise ValueError("surfel pyramid and dst_ranges hold different numbers of images")
+    elif dst_surfels is not None and tuple(dst_surfels.shape) != (dst.shape[0],) + hw + (4,):
+        raise ValueError(f"dst_surfels must be ({dst.shape[0]}, {hw[0]}, {hw[1]}, 4)")
+    if pair_src is not None and (pair_dst is None or pair_src.shape != pair_dst.shape):
+        raise ValueError("pair_src and pair_dst must be given together, with equal shapes")
     if dst_surfels is None:
         dst_surfels = normals_cross_batch(intr, dst, strides=[s for s, _ in config.schedule])
     B = src.shape[0] if pair_src is None else pair_src.shape[0]

@@ -923,3 +923,22 @@ def test_register_batch_stress_terminates(rk):
     st = res.status.cpu().numpy()
     assert set(np.unique(st)) <= {0, 1, 2} and (st == 2).any()
     assert torch.isfinite(res.poses).all()
+
+
+def test_register_batch_validates_inputs(rk, sensors):
+    """Shapes, dtypes and devices are checked on the host before any launch
+    (a mis-shaped pool would otherwise be read out of bounds)."""
+    import torch
+    intr = sensors["ouster"]
+    H, W = intr.height, intr.width
+    good = torch.zeros((2, H, W), dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, torch.zeros((2, W, H), device="cuda"), good)
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, good, good.double())
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, good.cpu(), good)
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, good, good, torch.zeros((2, H, W, 3), device="cuda"))
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, good, good, pair_src=torch.zeros(2, dtype=torch.int32, device="cuda"))
