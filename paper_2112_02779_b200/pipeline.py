@@ -68,6 +68,13 @@ def render_batch(intr: lm.LidarIntrinsics, scene, poses):
     return out
 
 
+def _check_frames(intr, frames):
+    t = nat.torch()
+    if not (nat.is_tensor(frames) and frames.is_cuda and frames.dtype == t.float32 and frames.ndim == 3
+            and tuple(frames.shape[1:]) == (intr.height, intr.width)):
+        raise ValueError(f"frames must be an (F, {intr.height}, {intr.width}) float32 CUDA tensor")
+
+
 @nvtx("integrate_sequence")
 def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, poses_w,
                        inv_w=None, clip_min: float = 0.0, clip_max: float = np.inf,
@@ -85,6 +92,9 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
     by the buffers) and replays it on later calls with the same buffers: the
     frame stamps live on the device, so a replay is an exact re-run.
     """
+    _check_frames(intr, frames)
+    if tuple(poses_w.shape) != (frames.shape[0], 12) or poses_w.dtype != nat.torch().float64:
+        raise ValueError("poses_w must be an (F, 12) float64 tensor")
     h = grid._prepare()
     sensor = lm.device_sensor(intr)
     radius = grid.truncation if radius is None else radius
@@ -144,6 +154,7 @@ def odometry(intr: lm.LidarIntrinsics, frames, config: RegistrationConfig = Regi
     relative registrations, or None when F < 2).
     """
     t = nat.torch()
+    _check_frames(intr, frames)
     F = int(frames.shape[0])
     if init not in ("identity", "centroid"):
         raise ValueError("init must be 'identity' or 'centroid'")
@@ -230,7 +241,10 @@ def eval_registration(intr: lm.LidarIntrinsics, frames, gt_poses, distances, pai
     number of pairs (the amortised per-pair cost of the batched launch)."""
     import time
     t = nat.torch()
+    _check_frames(intr, frames)
     F = int(frames.shape[0])
+    if len(gt_poses) != F:
+        raise ValueError("gt_poses must hold one pose per frame")
     jobs = []
     for d in distances:
         for k, (i, j) in enumerate(sample_pairs(F, int(d), pairs, seed=seed + int(d))):

@@ -332,8 +332,12 @@ def normals_cross_batch(intr: LidarIntrinsics, ranges, strides=None):
     """K1 over a (B, H, W) device batch -> (B, H, W, 4) surfel maps (batch
     API), or with ``strides`` a SurfelPyramid whose coarse levels the
     registration gathers from compact maps."""
-    B = ranges.shape[0]
     H, W = intr.height, intr.width
+    t = nat.torch()
+    if not (nat.is_tensor(ranges) and ranges.is_cuda and ranges.dtype == t.float32 and ranges.ndim == 3
+            and tuple(ranges.shape[1:]) == (H, W) and ranges.is_contiguous()):
+        raise ValueError(f"ranges must be a contiguous (B, {H}, {W}) float32 CUDA tensor")
+    B = ranges.shape[0]
     if strides is None:
         surf = nat.empty((B, H, W, 4), np.float32)
         nat.call("rk_normals_cross", lm.device_sensor(intr), nat.ptr(ranges), B, None, None,
