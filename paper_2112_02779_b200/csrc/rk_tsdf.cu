@@ -286,6 +286,15 @@ __global__ void __launch_bounds__(kAssignThreads) k_assign_slots(GridDev g) {
 #ifndef RK_TSDF_EARLY_STATE
 #define RK_TSDF_EARLY_STATE 1
 #endif
+#ifndef RK_TSDF_PREFETCH
+#define RK_TSDF_PREFETCH 0
+#endif
+
+// bulk L2 prefetch of one block's voxel states (TMA unit, no registers held)
+__device__ __forceinline__ void prefetch_block_l2(const float2* p) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(kVox * sizeof(float2)))
+               : "memory");
+}
 
 struct IntegrateArgs {
   GridDev g;
@@ -315,6 +324,13 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
   __shared__ int sh_e;
 #endif
   __shared__ RowTablesSmem sh_tab;
+#if RK_TSDF_STATIC && RK_TSDF_PREFETCH
+  // the first block's states stream into L2 while the lattice is built
+  if (threadIdx.x == 0 && blockIdx.x < (int)A.g.tc->n_touched) {
+    const int s0 = A.g.h_slot[A.g.touched[blockIdx.x]];
+    if (s0 >= 0) prefetch_block_l2(A.g.vox + (size_t)s0 * kVox);
+  }
+#endif
   if (SMEM) stage_tables(A.s, sh_tab, threadIdx.x, NT);
   const RowTables tb = SMEM ? RowTables{sh_tab.el32, sh_tab.az32, sh_tab.inv_rows} : global_tables(A.s);
   double R[9], t[3];
@@ -358,6 +374,10 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
       h_n = A.g.touched[e2];
       slot_n = A.g.h_slot[h_n];
       key_n = A.g.h_keys[h_n];
+#if RK_TSDF_PREFETCH
+      // the next block's states stream into L2 while this block runs
+      if (threadIdx.x == 0 && slot_n >= 0) prefetch_block_l2(A.g.vox + (size_t)slot_n * kVox);
+#endif
     }
     if (slot < 0) continue;
 #else
