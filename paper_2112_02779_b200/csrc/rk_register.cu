@@ -19,6 +19,7 @@
 // CTA-wide barrier) remain selectable with RK_ICP_WPP for experiments.
 #include "rk_common.cuh"
 #include "rk_linalg.cuh"
+#include <cooperative_groups.h>
 #if RK_ICP_TIME_SOLVE
 #include <cstdio>
 #endif
@@ -395,13 +396,24 @@ __device__ __forceinline__ void group_sync(int g) {
 
 // STATS: accumulate the robust cost and squared residuals (IterationStats
 // rows); the pose update needs neither, so batch runs without stats skip them.
-template <int MATH, int WPP, int MINB, bool SMEM, bool STATS, int NT = kThreads>
+//
+// CL > 1 (latency mode for a handful of pairs): one pair per thread-block
+// cluster of CL CTAs.  The point walk spans the cluster (walk index wtid over
+// WGT = CL * GT threads); each CTA reduces its slice as usual, then CTA rank 0
+// sums the CL partial systems through distributed shared memory in rank
+// order (deterministic), solves, and stores the pose and the control word
+// into every CTA's shared memory before the cluster barrier.
+template <int MATH, int WPP, int MINB, bool SMEM, bool STATS, int NT = kThreads, int CL = 1>
 __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
-  constexpr int NW = NT / 32, GROUPS = NW / WPP, GT = WPP * 32;
+  constexpr int NW = NT / 32, GROUPS = NW / WPP, GT = WPP * 32, WGT = GT * CL;
+  static_assert(CL == 1 || GROUPS == 1, "a cluster holds one pair");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp / WPP;
   const int gtid = tid - g * GT;
-  const int pair = blockIdx.x * GROUPS + g;
+  const int crank = CL > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const bool lead = crank == 0;  // the cluster CTA that solves and writes the outputs
+  const int wtid = crank * GT + gtid;
+  const int pair = CL > 1 ? (int)(blockIdx.x / CL) : blockIdx.x * GROUPS + g;
   const SensorDev& s = A.s;
   __shared__ RowTablesSmem sh_tab;
   if (SMEM) {
@@ -416,8 +428,8 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
   if ((A.cfg.n_src_images > 0 && (unsigned)ps >= (unsigned)A.cfg.n_src_images) ||
       (A.cfg.n_dst_images > 0 && (unsigned)pd >= (unsigned)A.cfg.n_dst_images)) {
     // an index outside the pools: no reads, a defined result (group-uniform exit)
-    if (gtid < 12) A.out12[pair * 12 + gtid] = A.init12[pair * 12 + gtid];
-    if (gtid == 0) {
+    if (lead && gtid < 12) A.out12[pair * 12 + gtid] = A.init12[pair * 12 + gtid];
+    if (lead && gtid == 0) {
       A.status[pair] = RK_ICP_BAD_PAIR;
       A.n_iters[pair] = 0;
     }
@@ -460,12 +472,12 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
     // row-major walk of the stride view (the reference's zero-copy StridedView,
     // range_image.py:69-116) by GT-point steps, as running pixel offsets:
     // one step advances (dv rows, du view columns), wrapping at Ws
-    const int dv = GT / Ws, du = GT - dv * Ws;
+    const int dv = WGT / Ws, du = WGT - dv * Ws;
     const int step_off = dv * stride * W + du * stride;
     const int wrap_off = stride * W - Ws * stride;
-    const int vi0 = gtid / Ws, ui0 = gtid - vi0 * Ws;
+    const int vi0 = wtid / Ws, ui0 = wtid - vi0 * Ws;
     const int off0 = vi0 * stride * W + ui0 * stride;
-    const bool col_mode = Ws % GT == 0;
+    const bool col_mode = Ws % WGT == 0;
     const int lvl_off = A.cfg.surfel_pitch ? A.cfg.surfel_level_off[lv] : 0;
     const int lvl_w = (A.cfg.surfel_pitch && lvl_off > 0) ? Ws : 0;
     const int row_step = stride * W;
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
     unsigned valid_lv = 0;
     if (A.pt_iters) {
       int off = off0, ui = ui0;
-      for (int k = gtid; k < npix; k += GT) {
+      for (int k = wtid; k < npix; k += WGT) {
         valid_lv += range_ok(__ldg(src + off), cmin, cmax) ? 1u : 0u;
         off += step_off;
         ui += du;
@@ -509,7 +521,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
         group_sync<WPP, NT>(g);
       }
       if (F32X && col_mode) {
-        for (int cj = gtid; cj < Ws; cj += GT) {
+        for (int cj = wtid; cj < Ws; cj += WGT) {
           const int u = cj * stride;
           const float4 o4 = __ldg(s.origins32 + u);
           const float* sp = src + u;
@@ -542,7 +554,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
       } else if (F32X) {
         // generic row-major walk, float32 transform
         int off = off0, ui = ui0;
-        for (int k = gtid; k < npix; k += GT) {
+        for (int k = wtid; k < npix; k += WGT) {
           const float r = __ldg(src + off);
           const float4 d4 = __ldg(s.dirs32 + off);
           const int u = ui * stride;
@@ -559,7 +571,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
         // column-owner walk (Ws % GT == 0): each lane owns view columns
         // gtid, gtid + GT, ... and walks them down the rows with a constant
         // pointer step; the receiver origin depends on the column only
-        for (int cj = gtid; cj < Ws; cj += GT) {
+        for (int cj = wtid; cj < Ws; cj += WGT) {
           const int u = cj * stride;
           const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
                                             __ldg(s.origins + 3 * u + 2));
@@ -586,19 +598,19 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
         int off = off0, ui = ui0;
         float r_next = 0.0f;
         double3 d_next = make_double3(0.0, 0.0, 0.0);
-        if (gtid < npix) {
+        if (wtid < npix) {
           r_next = __ldg(src + off);
           const double* dp = s.dirs + 3 * (size_t)off;
           d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
         }
-        for (int k = gtid; k < npix; k += GT) {
+        for (int k = wtid; k < npix; k += WGT) {
           const float r = r_next;
           const double3 dcur = d_next;
           const int u = ui * stride;
           off += step_off;
           ui += du;
           if (ui >= Ws) { ui -= Ws; off += wrap_off; }
-          if (k + GT < npix) {
+          if (k + WGT < npix) {
             r_next = __ldg(src + off);
             const double* dp = s.dirs + 3 * (size_t)off;
             d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
@@ -648,10 +660,27 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
       }
       group_sync<WPP, NT>(g);
+      if (CL > 1) {
+        // the cluster's partial systems -> the lead CTA, in rank order
+        cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        cl.sync();
+        if (lead && gtid <= kNumAcc) {
+          if (gtid < kNumAcc) {
+            double t = tot[gtid];
+            for (int r = 1; r < CL; ++r) t += cl.map_shared_rank(tot, r)[gtid];
+            tot[gtid] = t;
+          } else {
+            int c = sh_cnt[0];
+            for (int r = 1; r < CL; ++r) c += cl.map_shared_rank(&sh_cnt[0], r)[0];
+            sh_cnt[0] = c;
+          }
+        }
+        group_sync<WPP, NT>(g);
+      }
 #if RK_ICP_TRACE
       if (gtid == 0) printf("pair %d lv %d it %d reduced n %d\n", pair, lv, it, sh_cnt[g * WPP]);
 #endif
-      if (gtid < 32) {  // the group's first warp updates the pose
+      if (lead && gtid < 32) {  // the group's first warp updates the pose
         const int n_corr = sh_cnt[g * WPP];
         // (cfg fields by value: taking a kernel parameter's address would
         // spill the whole argument block to local memory)
@@ -683,8 +712,20 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           }
           sh_ctrl[g] = ctrl;
         }
+        if (CL > 1) {
+          // broadcast the pose and the control word to the other CTAs
+          __syncwarp();
+          cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+          for (int r = 1; r < CL; ++r) {
+            if (gtid < 12) cl.map_shared_rank(&sh_pose[0][0], r)[gtid] = sh_pose[0][gtid];
+            if (gtid == 12) cl.map_shared_rank(&sh_ctrl[0], r)[0] = sh_ctrl[0];
+          }
+        }
       }
-      group_sync<WPP, NT>(g);
+      if (CL > 1)
+        cooperative_groups::this_cluster().sync();
+      else
+        group_sync<WPP, NT>(g);
       const int ctrl = sh_ctrl[g];
 #if RK_ICP_TRACE
       if (gtid == 0) printf("pair %d lv %d it %d n %d ctrl %d t %.6f %.6f %.6f\n", pair, lv, it, sh_cnt[g * WPP], ctrl,
@@ -709,8 +750,8 @@ finish:
     if (lane == 0 && w) atomicAdd(A.pt_iters, (unsigned long long)w);
   }
   group_sync<WPP, NT>(g);
-  if (gtid < 12) A.out12[pair * 12 + gtid] = sh_pose[g][gtid];
-  if (gtid == 0) {
+  if (lead && gtid < 12) A.out12[pair * 12 + gtid] = sh_pose[g][gtid];
+  if (lead && gtid == 0) {
     A.status[pair] = status;
     A.n_iters[pair] = n_done;
   }
@@ -732,6 +773,62 @@ int launch(const IcpArgs& a, cudaStream_t st) {
     else
       k_register<MATH, WPP, MINB, false, false, NT><<<grid, NT, 0, st>>>(a);
   }
+  RK_LAUNCHED("k_register");
+  return RK_OK;
+}
+
+// latency mode over clusters: CL CTAs of NT threads per pair
+template <int CL, int NT = kWide>
+cudaLaunchConfig_t cluster_config(int batch, cudaStream_t st, cudaLaunchAttribute* at) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)batch * CL);
+  lc.blockDim = dim3(NT);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return lc;
+}
+
+// how many CL-CTA clusters are co-resident on this device (GPC packing:
+// 148 SMs do not hold 18 clusters of 8 full-SM CTAs); cached per device
+template <int CL>
+int max_active_clusters() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  if (!cache[dev]) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t lc = cluster_config<CL>(1, nullptr, at);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_register<MATH_FAST, kWide / 32, 1, true, false, kWide, CL>, &lc) !=
+            cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = -1;  // clusters unavailable: never chosen
+    }
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+template <int CL, int NT = kWide>
+int launch_cluster(const IcpArgs& a, cudaStream_t st) {
+  constexpr int WPP = NT / 32;
+  const bool smem = a.s.H <= kMaxRowsSmem && a.s.K <= kMaxInvSmem;
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t lc = cluster_config<CL, NT>(a.batch, st, at);
+  cudaError_t e;
+  if (a.stats)
+    e = smem ? cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, true, true, NT, CL>, a)
+             : cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, false, true, NT, CL>, a);
+  else
+    e = smem ? cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, true, false, NT, CL>, a)
+             : cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, false, false, NT, CL>, a);
+  if (e != cudaSuccess) return rk_cuda_status(e, "k_register (cluster)");
   RK_LAUNCHED("k_register");
   return RK_OK;
 }
@@ -807,6 +904,22 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
     if (nt == 512) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
   }
   if (!force && (!wide || atoi(wide))) {
+    // a few pairs: a cluster of CTAs per pair (RK_ICP_CLUSTER=0 disables,
+    // =2|4|8 forces the size)
+    const char* fcl = getenv("RK_ICP_CLUSTER");
+    const int want = fcl ? atoi(fcl) : -1;
+    if (want != 0) {
+      // the largest cluster whose batch fits in one wave of co-resident
+      // clusters (B200: 1-8 pairs x8, then x4, then <= 74 x2)
+      const int cl = want > 0 ? want
+                              : (batch <= max_active_clusters<8>()   ? 8
+                                 : batch <= max_active_clusters<4>() ? 4
+                                 : batch <= max_active_clusters<2>() ? 2
+                                                                     : 1);
+      if (cl == 8) return launch_cluster<8>(a, st);
+      if (cl == 4) return launch_cluster<4>(a, st);
+      if (cl == 2) return launch_cluster<2>(a, st);
+    }
     if (batch <= sm_count()) return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
     if (batch <= 2 * sm_count()) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
   }

@@ -322,6 +322,33 @@ def test_register_batch_layouts_match_reference(rk, wpp, sensors, golden_icp, mo
         assert rot_err(P.R, M[:3, :3]) < 1e-5 and np.linalg.norm(P.t - M[:3, 3]) < 1e-5
 
 
+@pytest.mark.parametrize("cluster", ("0", "2", "4", "8"))
+def test_register_latency_clusters_match_reference(rk, cluster, sensors, golden_icp, monkeypatch):
+    """Latency mode: one pair per 1024-thread CTA (0) or per cluster of 2/4/8
+    CTAs reducing through distributed shared memory -- same contract, and a
+    bad pair index still yields its defined status on every cluster size."""
+    import torch
+    from paper_2112_02779_b200.registration import ICP_BAD_PAIR
+    monkeypatch.setenv("RK_ICP_CLUSTER", cluster)
+    g, intr = golden_icp, sensors["ouster"]
+    src = torch.from_numpy(g["street/src"]).cuda()[None].repeat(2, 1, 1)
+    dst = torch.from_numpy(g["street/dst"]).cuda()[None].repeat(2, 1, 1)
+    ps = torch.tensor([0, 1, 5], dtype=torch.int32, device="cuda")
+    res = rk.register_batch(intr, src, dst, pair_src=ps, pair_dst=torch.tensor([1, 0, 0], dtype=torch.int32,
+                                                                                device="cuda"), with_stats=True)
+    M = g["street/reg_pose"]
+    st = g["street/reg_stats"]
+    for b in range(2):
+        assert int(res.status[b]) == 0
+        assert int(res.iterations[b]) == st.shape[0]
+        P = res.pose(b)
+        assert rot_err(P.R, M[:3, :3]) < 1e-5 and np.linalg.norm(P.t - M[:3, 3]) < 1e-5
+        got = res.stats[b, :st.shape[0]].cpu().numpy()
+        assert np.array_equal(got[:, :2], st[:, :2])  # stride, iteration
+        assert np.all(np.abs(got[:, 2] - st[:, 2]) <= np.maximum(2, 1e-3 * st[:, 2]))
+    assert int(res.status[2]) == ICP_BAD_PAIR and int(res.iterations[2]) == 0
+
+
 def test_register_nonconvergence_and_identity(rk, sensors, golden_icp):
     intr = sensors["synth"]
     img = rk.RangeImage(golden_icp["synth/dst"], intr)
