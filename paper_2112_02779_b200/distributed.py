@@ -139,12 +139,19 @@ class ShardedGrid:
         two graph launches and one collective instead of ~4F kernel launches
         (at 8 ranks the per-rank GPU work of a 100-frame sequence is shorter
         than issuing those launches).  ``reduce`` overrides the collective
-        (tests emulate several shards in one process)."""
+        (tests emulate several shards in one process).
+
+        The caller presizes the pool (``self.grid.reserve``): unlike the
+        single-GPU per-frame API there is no grow-and-retry here, so an
+        activation that overflows raises DeviceError (checked after eager
+        activations and after the first replay of a recorded graph).
+        Returns the device int64 updated-voxel counter."""
         from . import lidar_model as lm
         g = self.grid
         h = g._prepare()
         sensor = lm.device_sensor(intr)
-        if updated is None:
+        own_upd = updated is None
+        if own_upd:
             updated = nat.zeros((1,), np.int64)
         F = int(frames.shape[0])
         cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
@@ -157,11 +164,17 @@ class ShardedGrid:
             g._graphs.clear()
             self._slots = F
         nat.call("rk_grid_reserve_slots", h, F, nat.stream_ptr())
+        # a counter this call allocates is owned by the cache entry (zeroed
+        # per replay), so it does not key the cache
         key = ("sharded", sensor, frames.data_ptr(), F, poses_w.data_ptr(), inv_w.data_ptr(),
-               updated.data_ptr(), cmin, cmax, lm.default_math())
+               None if own_upd else updated.data_ptr(), cmin, cmax, lm.default_math())
         bufs = g._graphs.get(key) if graph else None
         if bufs is None:
-            bufs = dict(stats=nat.zeros((F, 2), np.int64), glob=nat.zeros((F, 2), np.int64))
+            bufs = dict(stats=nat.zeros((F, 2), np.int64), glob=nat.zeros((F, 2), np.int64),
+                        upd=updated)
+        elif own_upd:
+            bufs["upd"].zero_()
+        upd = bufs["upd"]
 
         def activate():
             st = nat.stream_ptr()
@@ -173,10 +186,16 @@ class ShardedGrid:
         def integrate():
             nat.call("rk_grid_integrate_activated", h, sensor, nat.ptr(frames), F, nat.ptr(inv_w),
                      nat.ptr(bufs["glob"]) if sharded else None, cmin, cmax, lm.default_math(),
-                     nat.ptr(updated), nat.stream_ptr())
+                     nat.ptr(upd), nat.stream_ptr())
 
+        # The pool must be presized (grid.reserve): an activation that runs
+        # out of slots leaves new blocks unallocated and K5 would skip them,
+        # so the overflow flag is checked after every eager activation and
+        # after the first replay of a freshly recorded graph, before any
+        # integration runs.
         if not graph:
             activate()
+            g.check_overflow()
             if sharded:
                 bufs["glob"].copy_(red(bufs["stats"]))
             integrate()
@@ -191,13 +210,16 @@ class ShardedGrid:
                         fn()
                     bufs[name] = gr
                 torch.cuda.current_stream().wait_stream(side)
-                g._graphs[key] = bufs
-            bufs["ga"].replay()
+                g.cache_graph(key, bufs)
+                bufs["ga"].replay()
+                g.check_overflow()
+            else:
+                bufs["ga"].replay()
             if sharded:
                 bufs["glob"].copy_(red(bufs["stats"]))
             bufs["gi"].replay()
         g.blocks._bump()
-        return updated
+        return upd.clone() if own_upd else upd
 
     def extract_mesh(self, min_weight: float = 1.0):
         """Distributed marching cubes: one all-to-all of halo blocks, MC on the

@@ -98,11 +98,12 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
     h = grid._prepare()
     sensor = lm.device_sensor(intr)
     radius = grid.truncation if radius is None else radius
-    if inv_w is None:
+    own_inv, own_upd = inv_w is None, updated is None
+    if own_inv:
         host = nat.to_host(poses_w)
         inv_w = nat.to_dev(np.stack([RigidTransform(r[:9].reshape(3, 3), r[9:]).inverse().as_row12()
                                      for r in host]), np.float64)
-    if updated is None:
+    if own_upd:
         updated = nat.zeros((1,), np.int64)
     cmin, cmax = float(np.float32(clip_min)), float(np.float32(clip_max))
     math = lm.default_math()
@@ -111,29 +112,40 @@ def integrate_sequence(grid: VoxelBlockGrid, intr: lm.LidarIntrinsics, frames, p
     poses_w = poses_w.contiguous()
     inv_w = inv_w.contiguous()
 
-    def issue():
+    def issue(inv, upd):
         # activation of frame f+1 overlaps the integration of frame f
         nat.call("rk_grid_integrate_frames", h, sensor, nat.ptr(frames), int(frames.shape[0]),
-                 nat.ptr(poses_w), nat.ptr(inv_w), float(radius), cmin, cmax, math,
-                 nat.ptr(updated), nat.stream_ptr())
+                 nat.ptr(poses_w), nat.ptr(inv), float(radius), cmin, cmax, math,
+                 nat.ptr(upd), nat.stream_ptr())
 
     if not graph:
-        issue()
+        issue(inv_w, updated)
     else:
-        # graphs live on the grid (dropped when its tables are reallocated)
+        # graphs live on the grid (dropped when its tables are reallocated).
+        # Buffers this function allocates itself (inverse poses, counter) are
+        # owned by the cache entry and refilled per call, so they do not key
+        # the cache: repeated calls replay one graph instead of recording a
+        # new one per call.
         key = (sensor, frames.data_ptr(), tuple(frames.shape), poses_w.data_ptr(),
-               inv_w.data_ptr(), updated.data_ptr(), float(radius), cmin, cmax, math)
-        g = grid._graphs.get(key)
-        if g is None:
+               None if own_inv else inv_w.data_ptr(), None if own_upd else updated.data_ptr(),
+               float(radius), cmin, cmax, math)
+        ent = grid._graphs.get(key)
+        if ent is None:
             torch = nat.torch()
-            g = torch.cuda.CUDAGraph()
+            ent = dict(inv=inv_w, upd=updated, g=torch.cuda.CUDAGraph())
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
-                issue()
+            with torch.cuda.graph(ent["g"], stream=side, capture_error_mode="thread_local"):
+                issue(ent["inv"], ent["upd"])
             torch.cuda.current_stream().wait_stream(side)
-            grid._graphs[key] = g
-        g.replay()
+            grid.cache_graph(key, ent)
+        else:
+            if own_inv:
+                ent["inv"].copy_(inv_w)
+            if own_upd:
+                ent["upd"].zero_()
+        ent["g"].replay()
+        updated = ent["upd"].clone() if own_upd else updated
     grid.blocks._bump()
     return updated
 

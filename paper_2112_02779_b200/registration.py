@@ -249,6 +249,16 @@ class BatchResult:
         return RigidTransform(p[:9].reshape(3, 3), p[9:])
 
 
+def _pair_index(x, name: str, B: int):
+    """Validate a (B,) int32/int64 CUDA index tensor; return a contiguous
+    int32 tensor the caller keeps alive across the launch."""
+    t = nat.torch()
+    if not (nat.is_tensor(x) and x.is_cuda and x.ndim == 1 and x.dtype in (t.int32, t.int64)
+            and int(x.shape[0]) == B and B >= 0):
+        raise ValueError(f"{name} must be a 1-D int32/int64 CUDA tensor of the batch length")
+    return x.to(t.int32).contiguous()
+
+
 @nvtx("register_batch")
 def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels=None,
                    pair_src=None, pair_dst=None, inits=None,
@@ -278,19 +288,28 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
             raise ValueError("surfel pyramid and dst_ranges hold different numbers of images")
     elif dst_surfels is not None and tuple(dst_surfels.shape) != (dst.shape[0],) + hw + (4,):
         raise ValueError(f"dst_surfels must be ({dst.shape[0]}, {hw[0]}, {hw[1]}, 4)")
-    if pair_src is not None and (pair_dst is None or pair_src.shape != pair_dst.shape):
-        raise ValueError("pair_src and pair_dst must be given together, with equal shapes")
+    if (pair_src is None) != (pair_dst is None):
+        raise ValueError("pair_src and pair_dst must be given together")
     if dst_surfels is None:
         dst_surfels = normals_cross_batch(intr, dst, strides=[s for s, _ in config.schedule])
-    B = src.shape[0] if pair_src is None else pair_src.shape[0]
+    B = int(src.shape[0]) if pair_src is None else \
+        (int(pair_src.shape[0]) if getattr(pair_src, "ndim", 0) == 1 else -1)
     dev = nat.device()
     if pair_src is None:
         pair_src = t.arange(B, dtype=t.int32, device=dev)
-    if pair_dst is None:
         pair_dst = t.arange(B, dtype=t.int32, device=dev)
+    # the int32 copies stay bound to locals until the launch has been issued:
+    # a temporary freed inside the argument list could be recycled by the
+    # next conversion before the kernel reads it
+    pair_src = _pair_index(pair_src, "pair_src", B)
+    pair_dst = _pair_index(pair_dst, "pair_dst", B)
     if inits is None:
         inits = t.zeros((B, 12), dtype=t.float64, device=dev)
         inits[:, 0] = inits[:, 4] = inits[:, 8] = 1.0
+    elif not (nat.is_tensor(inits) and inits.is_cuda and inits.dtype == t.float64
+              and tuple(inits.shape) == (B, 12)):
+        raise ValueError(f"inits must be a ({B}, 12) float64 CUDA tensor")
+    inits = inits.contiguous()
     poses = t.empty((B, 12), dtype=t.float64, device=dev)
     status = t.empty((B,), dtype=t.int32, device=dev)
     iters = t.empty((B,), dtype=t.int32, device=dev)
@@ -308,8 +327,7 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
             cfg.surfel_level_off[i] = int(dst_surfels.offsets[int(s)])
         surf = dst_surfels.data
     nat.call("rk_register_batch", lm.device_sensor(intr), nat.ptr(src), nat.ptr(dst),
-             nat.ptr(surf), nat.ptr(pair_src.to(t.int32).contiguous()),
-             nat.ptr(pair_dst.to(t.int32).contiguous()), B, nat.ptr(inits.contiguous()),
+             nat.ptr(surf), nat.ptr(pair_src), nat.ptr(pair_dst), B, nat.ptr(inits),
              C.byref(cfg), nat.ptr(poses), nat.ptr(status), nat.ptr(iters),
              nat.ptr(stats), max_it if with_stats else 0, nat.ptr(pt_iters), nat.stream_ptr())
     return BatchResult(poses, status, iters, stats)

@@ -20,7 +20,7 @@ import numpy as np
 from . import _native as nat
 from .trace import nvtx
 from . import lidar_model as lm
-from .errors import InvalidPose
+from .errors import DeviceError, InvalidPose
 from .range_image import RangeImage
 from .se3 import RigidTransform
 
@@ -235,6 +235,24 @@ class VoxelBlockGrid:
                 self._lib.rk_grid_destroy(self._handle)
             except Exception:
                 pass
+
+    MAX_GRAPHS = 32
+
+    def cache_graph(self, key, entry):
+        """Keep a recorded CUDA graph (bounded: the oldest entry is dropped
+        beyond MAX_GRAPHS, so callers passing fresh buffers cannot grow the
+        cache without limit)."""
+        while len(self._graphs) >= self.MAX_GRAPHS:
+            self._graphs.pop(next(iter(self._graphs)))
+        self._graphs[key] = entry
+
+    def check_overflow(self):
+        """Raise if an activation ran out of pool capacity (new blocks got no
+        slot and were skipped) -- synchronises."""
+        n_blocks, cap, overflow, _ = self.info()
+        if overflow:
+            raise DeviceError(f"voxel-block pool overflow: {n_blocks} blocks in a pool of {cap}; "
+                              f"call grid.reserve() with a larger capacity before integrating")
 
     def info(self):
         """(n_blocks, capacity, overflowed, n_touched) -- synchronises."""

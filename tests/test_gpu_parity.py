@@ -267,6 +267,59 @@ def test_register_batch_deterministic_and_consistent(rk, sensors, golden_icp):
     assert np.array_equal(a.pose(0).matrix(), single.pose.matrix())
 
 
+def test_register_batch_index_dtypes_and_validation(rk, sensors, golden_icp):
+    """int64 pair indices (torch's default) give the same poses as int32 ones
+    (the converted copies stay alive across the launch), and host-side or
+    mis-shaped index / init tensors are rejected before any launch."""
+    import torch
+    g, intr = golden_icp, sensors["ouster"]
+    src = torch.from_numpy(np.stack([g["street/src"], g["street/dst"]])).cuda()
+    dst = torch.from_numpy(np.stack([g["street/dst"], g["street/src"]])).cuda()
+    ps64 = torch.tensor([0, 1, 0, 1], dtype=torch.int64, device="cuda")
+    pd64 = torch.tensor([0, 0, 1, 1], dtype=torch.int64, device="cuda")
+    a = rk.register_batch(intr, src, dst, pair_src=ps64, pair_dst=pd64)
+    b = rk.register_batch(intr, src, dst, pair_src=ps64.int(), pair_dst=pd64.int())
+    assert torch.equal(a.poses, b.poses) and torch.equal(a.status, b.status)
+    # pair 0 = (src 0, dst 0) is the golden street pair; pair 1 = (dst image, dst image)
+    single = rk.register(rk.RangeImage(g["street/src"], intr), rk.RangeImage(g["street/dst"], intr))
+    assert np.abs(a.pose(0).matrix() - single.pose.matrix()).max() < 1e-5
+    assert np.abs(a.pose(1).matrix() - np.eye(4)).max() < 1e-6
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, pair_src=ps64.cpu(), pair_dst=pd64)
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, pair_src=ps64, pair_dst=pd64[:3])
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, pair_src=None, pair_dst=pd64)
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, pair_src=ps64, pair_dst=pd64,
+                          inits=torch.zeros((3, 12), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, pair_src=ps64, pair_dst=pd64,
+                          inits=torch.zeros((4, 12), dtype=torch.float64))
+
+
+@pytest.mark.parametrize("batch", [1, 2, 8, 9, 17, 18, 19, 37, 38, 74, 75, 148, 149, 300])
+def test_register_batch_tiers_match_register(rk, sensors, golden_icp, batch):
+    """The launcher picks a cluster size (x8/x4/x2) or CTA width (1024/512/256)
+    from the batch size, which changes each pair's float32 per-thread split,
+    so results may differ in the last bits between tiers (INTEGRATION.md,
+    'Batch-size dependence').  Every tier stays inside the pose contract
+    (1e-5) of the single-pair register() on the golden street pair, with
+    the same per-pair iteration count."""
+    import torch
+    g, intr = golden_icp, sensors["ouster"]
+    src = torch.from_numpy(g["street/src"]).cuda()[None]
+    dst = torch.from_numpy(g["street/dst"]).cuda()[None]
+    zeros = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    res = rk.register_batch(intr, src, dst, pair_src=zeros, pair_dst=zeros)
+    single = rk.register(rk.RangeImage(g["street/src"], intr), rk.RangeImage(g["street/dst"], intr))
+    P = res.poses.cpu().numpy()
+    ref = single.pose.as_row12()
+    assert np.abs(P - ref[None]).max() < 1e-5
+    assert bool((res.poses == res.poses[:1]).all())      # one tier per launch: all pairs equal
+    assert set(res.iterations.cpu().tolist()) == {len(single.stats)}
+
+
 @pytest.mark.parametrize("pair", PAIRS)
 def test_register_batch_surfel_pyramid_bitidentical(rk, pair, sensors, golden_icp):
     """Coarse levels gathering from the decimated surfel maps see exactly the
@@ -488,6 +541,49 @@ def test_integrate_sequence_graph_replay_matches_eager(rk, sensors, golden_icp):
     assert len(out_grid._graphs) == 1          # recorded once, replayed once
     for n, keys, vox in out[1:]:
         assert n == out[0][0] and keys == out[0][1] and np.array_equal(vox, out[0][2])
+
+
+def test_integrate_sequence_graph_cache_owns_its_buffers(rk, sensors):
+    """graph=True without caller-provided inverse poses / counter: the cache
+    entry owns those buffers, so repeated calls replay ONE graph (the cache
+    does not grow per call) and each call returns a fresh count equal to the
+    eager run's; the cache is bounded by VoxelBlockGrid.MAX_GRAPHS."""
+    import torch
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = sensors["ouster"]
+    traj = scenes.street_trajectory(4, seed=1)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    poses = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    grid = rk.VoxelBlockGrid(voxel_size=0.05, capacity=8192)
+    ref = int(pipeline.integrate_sequence(grid, intr, frames, poses, clip_max=30.0).item())
+    counts = []
+    for _ in range(3):
+        pipeline.clear_grid(grid)
+        counts.append(pipeline.integrate_sequence(grid, intr, frames, poses, clip_max=30.0, graph=True))
+    assert len(grid._graphs) == 1
+    assert [int(c.item()) for c in counts] == [ref] * 3
+    assert len({c.data_ptr() for c in counts}) == 3       # kept results are not overwritten
+    for i in range(grid.MAX_GRAPHS + 3):
+        grid.cache_graph(("probe", i), None)
+    assert len(grid._graphs) == grid.MAX_GRAPHS
+
+
+def test_sharded_grid_overflow_raises(rk, sensors):
+    """ShardedGrid.integrate_frames with an undersized pool raises instead of
+    silently skipping the unallocated blocks (eager and on the first replay
+    of a recorded graph)."""
+    import torch
+    from paper_2112_02779_b200 import pipeline, scenes
+    from paper_2112_02779_b200.distributed import ShardedGrid
+    intr = sensors["ouster"]
+    traj = scenes.street_trajectory(2, seed=0)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    poses = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    inv = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).cuda()
+    for graph in (False, True):
+        sg = ShardedGrid(0.05, 0, 1, capacity=64)
+        with pytest.raises(rk.DeviceError, match="overflow"):
+            sg.integrate_frames(intr, frames, poses, inv, clip_max=30.0, graph=graph)
 
 
 def test_hash_sharded_grid_equals_single_grid(rk, sensors, golden_icp):
