@@ -61,6 +61,9 @@ def parse():
     # TSDF sequence shape: c2 (default; 64x1024 Ouster-like, 5 cm), c3 (HDL-64
     # 64x2048, 10 cm), c5 (OS-128 128x2048, 3 cm) -- BASELINE.json configs
     ap.add_argument("--tsdf-config", default="c2", choices=["c2", "c3", "c5"])
+    # projection arithmetic: np = numpy-exact (the reference's bits), fast =
+    # minimax transcendentals + float32 ICP move, cr = correctly rounded
+    ap.add_argument("--math", default=None, choices=["np", "fast", "cr"])
     # diagnostic only (not a bench configuration): every pair reads pool image 0's
     # destination, isolating the cost of the data-dependent surfel gather
     ap.add_argument("--diag-same-dst", action="store_true")
@@ -588,6 +591,9 @@ def main():
         return
 
     dist, rank, world = dist_init(args)
+    if args.math is not None:
+        from paper_2112_02779_b200 import lidar_model as lm
+        lm.set_default_math({"np": lm.MATH_NP, "fast": lm.MATH_FAST, "cr": lm.MATH_CR}[args.math])
     import torch
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")

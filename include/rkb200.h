@@ -39,10 +39,13 @@ enum {
 };
 
 /* math modes of the float32 projection:
- * FAST = minimax atan2/asin + reciprocal refinements (default), CR = float64
- * transcendentals rounded once (bit-comparable with the oracle), LIBM = CUDA's
- * accurate atan2f/asinf with IEEE division (only rk_project_f32 accepts it). */
-enum { RK_MATH_FAST = 0, RK_MATH_CR = 1, RK_MATH_LIBM = 2 };
+ * FAST = minimax atan2/asin + reciprocal refinements (and a float32 ICP move),
+ * CR = float64 transcendentals rounded once (bit-comparable with the oracle's
+ * math="cr"), LIBM = CUDA's accurate atan2f/asinf with IEEE division (only
+ * rk_project_f32 accepts it), NP = numpy's own float32 arctan2/arcsin (the
+ * SVML sequences restated bit for bit) with exact arithmetic everywhere else:
+ * the reference's projection (lidar_model.py:262-344) bit for bit. */
+enum { RK_MATH_FAST = 0, RK_MATH_CR = 1, RK_MATH_LIBM = 2, RK_MATH_NP = 3 };
 
 /* per-pair ICP status (registration.py:266-272) */
 enum { RK_ICP_CONVERGED = 0, RK_ICP_TOO_FEW = 1, RK_ICP_DEGENERATE = 2, RK_ICP_BAD_PAIR = 3 };
@@ -79,6 +82,11 @@ int rk_sensor_destroy(rk_sensor* s);
 /* project_many(single=True, refine=False)  lidar_model.py:262-344 */
 int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, int math,
                    float* u, int32_t* v, float* r, int8_t* status, void* stream);
+/* diagnostic: RK_MATH_NP's transcendentals elementwise on device arrays --
+ * fn 0: out = np.arctan2(a, b) (lidar_model.py:288), fn 1: out = np.arcsin(a)
+ * (lidar_model.py:45; |a| <= 1), float32 (parity tests against numpy) */
+int rk_svml_eval(const rk_sensor* s, int fn, const float* a, const float* b, int64_t n,
+                 float* out, void* stream);
 /* project_many(single=False) float64 fixed-point path, lidar_model.py:287-344.
  * work: caller scratch of >= 3*n doubles + 16 bytes. */
 int rk_project_f64(const rk_sensor* s, const double* pts, int64_t n, int max_iters,

@@ -96,11 +96,60 @@ def rows_times_mat_t(points, M, t=None, mode="exact"):
     return np.stack(cols, axis=-1)
 
 
+_svml_lib = None
+
+
+def _svml():
+    """oracle/svml_emu.c (numpy's SVML float32 arctan2 / arcsin restated in C),
+    compiled on first use into oracle/_build/ with the host's gcc."""
+    global _svml_lib
+    if _svml_lib is None:
+        import ctypes
+        import subprocess
+        from pathlib import Path
+        here = Path(__file__).resolve().parent
+        src = here / "svml_emu.c"
+        so = here / "_build" / "libsvml_emu.so"
+        if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
+            so.parent.mkdir(exist_ok=True)
+            subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", str(src), "-o",
+                            str(so), "-lm"], check=True)
+        lib = ctypes.CDLL(str(so))
+        lib.svml_atan2f_n.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_long]
+        lib.svml_asinf_n.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_long]
+        tab = np.fromfile(here.parent / "paper_2112_02779_b200" / "data" / "vrsqrt14.u16", dtype="<u2")
+        _svml_lib = (lib, np.ascontiguousarray(tab))
+    return _svml_lib
+
+
+def svml_atan2(y, x):
+    """numpy's AVX-512 float32 arctan2, host-independent (svml_emu.c)."""
+    lib, _ = _svml()
+    y, x = np.broadcast_arrays(np.asarray(y, dtype=np.float32), np.asarray(x, dtype=np.float32))
+    y, x = np.ascontiguousarray(y), np.ascontiguousarray(x)
+    out = np.empty(y.shape, np.float32)
+    lib.svml_atan2f_n(y.ctypes.data, x.ctypes.data, out.ctypes.data, y.size)
+    return out
+
+
+def svml_asin(q):
+    """numpy's AVX-512 float32 arcsin, host-independent (svml_emu.c)."""
+    lib, tab = _svml()
+    q = np.ascontiguousarray(np.asarray(q, dtype=np.float32))
+    out = np.empty(q.shape, np.float32)
+    lib.svml_asinf_n(q.ctypes.data, tab.ctypes.data, out.ctypes.data, q.size)
+    return out
+
+
 def atan2_f32(y, x, math="numpy"):
+    """math: "numpy" (the host's own np.arctan2, what the reference runs),
+    "svml" (numpy's AVX-512 result on any host), "cr" (correctly rounded)."""
     y = np.asarray(y, dtype=np.float32)
     x = np.asarray(x, dtype=np.float32)
     if math == "numpy":
         return np.arctan2(y, x)
+    if math == "svml":
+        return svml_atan2(y, x)
     return np.arctan2(y.astype(np.float64), x.astype(np.float64)).astype(np.float32)
 
 
@@ -108,4 +157,6 @@ def asin_f32(q, math="numpy"):
     q = np.asarray(q, dtype=np.float32)
     if math == "numpy":
         return np.arcsin(q)
+    if math == "svml":
+        return svml_asin(q)
     return np.arcsin(q.astype(np.float64)).astype(np.float32)

@@ -50,24 +50,36 @@ def activate(grid, points, radius, extent):
     return touched
 
 
-def _chunk_centres(keys, R_inv, t_inv, voxel, fma="exact"):
+def _chunk_centres(keys, R_inv, t_inv, voxel, fma="exact", lone=None):
     """Sensor-frame voxel centres of a chunk of blocks (lines 157-161).
 
     base (float64, one row per block) and the rotated local lattice are rounded
-    to float32 separately and summed in float32.
+    to float32 separately and summed in float32.  A chunk
+    of ONE block goes through dgemv, whose FMA order differs (exactmath);
+    ``lone`` overrides whether this chunk is such a lone block (None: decided
+    by the chunk's own length).
     """
     kb = np.asarray(keys, dtype=np.float64).reshape(-1, 3) * (EDGE * voxel)
-    base = rows_times_mat_t(kb, R_inv, t_inv, mode=fma)
+    if lone is False and kb.shape[0] == 1:
+        base = rows_times_mat_t(np.repeat(kb, 2, axis=0), R_inv, t_inv, mode=fma)[:1]
+    else:
+        base = rows_times_mat_t(kb, R_inv, t_inv, mode=fma)
     off = rows_times_mat_t((LOCAL + 0.5) * voxel, R_inv, None, mode=fma).astype(F32)
     return (base.astype(F32)[:, None, :] + off[None, :, :]).reshape(-1, 3)
 
 
 def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
-              free_space=True, clip_min=0.0, clip_max=np.inf, math="numpy", fma="exact"):
+              free_space=True, clip_min=0.0, clip_max=np.inf, math="numpy", fma="exact",
+              touched=None):
     """Projective running-average update of the given blocks (lines 116-186).
 
     (R, t) maps the frame into the world; its inverse is formed with numpy as
     the reference does (se3.py:72-74).  Returns the number of updated voxels.
+
+    ``touched``: integrate only ``keys`` but with the arithmetic each block
+    gets inside this larger touched set (the reference chunks the sorted set
+    in 146-block tasks; only a lone last block is computed differently), so a
+    sample of blocks can be checked without integrating the whole frame.
     """
     R = np.asarray(R, dtype=float)
     t = np.asarray(t, dtype=float)
@@ -78,9 +90,20 @@ def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
     W = sensor.W
     tau = F32(trunc)
     updated = 0
-    for i0 in range(0, len(order), CHUNK_BLOCKS):
-        part = order[i0:i0 + CHUNK_BLOCKS]
-        x = _chunk_centres(part, R_inv, t_inv, voxel, fma=fma)
+    lone_key = None
+    if touched is None:
+        chunks = [order[i0:i0 + CHUNK_BLOCKS] for i0 in range(0, len(order), CHUNK_BLOCKS)]
+    else:
+        full = sorted(touched)
+        lone_key = full[-1] if len(full) % CHUNK_BLOCKS == 1 else None
+        # every block but the lone one in multi-row chunks
+        rest = [k for k in order if k != lone_key]
+        chunks = [rest[i0:i0 + CHUNK_BLOCKS] for i0 in range(0, len(rest), CHUNK_BLOCKS)]
+        if lone_key is not None and lone_key in set(order):
+            chunks.append([lone_key])
+    for part in chunks:
+        lone = None if touched is None else (part == [lone_key])
+        x = _chunk_centres(part, R_inv, t_inv, voxel, fma=fma, lone=lone)
         u, v, r, status = sensor.project_f32(x, math=math)
         col = (u + F32(0.5)).astype(np.int32)
         col[col == W] = 0

@@ -50,6 +50,7 @@ SIGNATURES = {
     "rk_sensor_create": [C.POINTER(SensorDesc), C.POINTER(_p)],
     "rk_sensor_destroy": [_p],
     "rk_project_f32": [_p, _p, _i64, C.c_int, _p, _p, _p, _p, _p],
+    "rk_svml_eval": [_p, C.c_int, _p, _p, _i64, _p, _p],
     "rk_project_f64": [_p, _p, _i64, C.c_int, _f64, C.c_int, _p, _p, _p, _p, _p, _p],
     "rk_row_from_elevation": [_p, _p, C.c_int, _i64, _p, _p],
     "rk_inverse_lut_lookup": [_p, _i32, _f64, _f64, _p, C.c_int, _i64, _p, _p],

@@ -75,6 +75,9 @@ extern "C" int rk_correspondences_f32(const rk_sensor* s, const double* src_pts,
   if (math == MATH_CR)
     k_correspondences<MATH_CR><<<blocks, 256, 0, S(stream)>>>(s->dev, src_pts, n, surf, pose12, gate2,
                                                               stride, inv_s, keep, target, normal);
+  else if (math == MATH_NP)
+    k_correspondences<MATH_NP><<<blocks, 256, 0, S(stream)>>>(s->dev, src_pts, n, surf, pose12, gate2,
+                                                              stride, inv_s, keep, target, normal);
   else
     k_correspondences<MATH_FAST><<<blocks, 256, 0, S(stream)>>>(s->dev, src_pts, n, surf, pose12, gate2,
                                                                 stride, inv_s, keep, target, normal);

@@ -26,6 +26,9 @@
 
 using namespace rk;
 
+#ifndef RK_ICP_MINB_NP  // CTAs per SM for the numpy-exact kernel
+#define RK_ICP_MINB_NP 4
+#endif
 #ifndef RK_ICP_MINB
 #define RK_ICP_MINB 4
 #endif
@@ -34,6 +37,11 @@ using namespace rk;
 #endif
 #ifndef RK_ICP_FUSED
 #define RK_ICP_FUSED 1
+#endif
+// RK_ICP_F64_AHEAD (exact modes' float64 walk): hold the next row's float64
+// ray in registers (1) or load the ray and origin at use (0)
+#ifndef RK_ICP_F64_AHEAD
+#define RK_ICP_F64_AHEAD 1
 #endif
 #ifndef RK_ICP_ELEV_ONLY
 #define RK_ICP_ELEV_ONLY 1
@@ -241,9 +249,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 // roundings, so MATH_CR associates exactly like the oracle.
 // q: the association target {x, y, z} (registration.py:168-176), from the
 // surfel pyramid record or formed from the ray tables by the caller.
-template <bool STATS, bool FUSED = false>
+// EXACT_COST (the exact modes): the IterationStats cost term is the
+// reference's own expression 1/w - 1 with w = 1 / sqrt(1 + (r/k)^2) in
+// float32 (registration.py:350-352, 357-358), cancellation included.
+template <bool STATS, bool FUSED = false, bool EXACT_COST = false>
 __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, const float4& n,
-                                                 const float4& q, float gate2, float inv_k,
+                                                 const float4& q, float gate2, float inv_k, float k32,
                                                  float* acc, float& cost, float& sumsq, int& cnt) {
   if (!(n.w > 0.0f)) return;  // stored range > 0 and normal valid
   float dx, dy, dz, d2, res;
@@ -289,8 +300,14 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
 #pragma unroll
   for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
   if (STATS) {
-    // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
-    cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
+    if (EXACT_COST) {
+      const float ek = __fdiv_rn(res, k32);
+      const float wx = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(1.0f, __fmul_rn(ek, ek))));
+      cost = __fadd_rn(cost, __fsub_rn(__fdiv_rn(1.0f, wx), 1.0f));
+    } else {
+      // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
+      cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
+    }
     sumsq = __fmaf_rn(res, res, sumsq);
   }
   ++cnt;
@@ -300,7 +317,7 @@ template <int MATH, bool SMEM, bool STATS>
 __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTables& tb, float mx,
                                                 float my, float mz, const float4* surf, bool lvl_rec,
                                                 int stride, int lvl_off, int lvl_w, float inv_s,
-                                                float gate2, float inv_k, float* acc, float& cost,
+                                                float gate2, float inv_k, float k32, float* acc, float& cost,
                                                 float& sumsq, int& cnt);
 
 __device__ __forceinline__ void prefetch_line(const void* p) {
@@ -326,14 +343,14 @@ __device__ __forceinline__ void associate_point(const SensorDev& s, const RowTab
                                                 const double* pose, float r, const double3& dcur,
                                                 const double3& ocur, const float4* surf, bool lvl_rec,
                                                 int stride, int lvl_off, int lvl_w, float inv_s,
-                                                float gate2, float inv_k, float* acc, float& cost,
+                                                float gate2, float inv_k, float k32, float* acc, float& cost,
                                                 float& sumsq, int& cnt) {
   const double rd = (double)r;
   double m[3];
   xform_rows(pose, pose + 9, __dadd_rn(__dmul_rn(rd, dcur.x), ocur.x),
              __dadd_rn(__dmul_rn(rd, dcur.y), ocur.y), __dadd_rn(__dmul_rn(rd, dcur.z), ocur.z), m);
   associate_moved<MATH, SMEM, STATS>(s, tb, (float)m[0], (float)m[1], (float)m[2], surf, lvl_rec, stride, lvl_off,
-                                     lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
+                                     lvl_w, inv_s, gate2, inv_k, k32, acc, cost, sumsq, cnt);
 }
 
 // the association of an already transformed (float32) source point
@@ -341,7 +358,7 @@ template <int MATH, bool SMEM, bool STATS>
 __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTables& tb, float mx,
                                                 float my, float mz, const float4* surf, bool lvl_rec,
                                                 int stride, int lvl_off, int lvl_w, float inv_s,
-                                                float gate2, float inv_k, float* acc, float& cost,
+                                                float gate2, float inv_k, float k32, float* acc, float& cost,
                                                 float& sumsq, int& cnt) {
   const Proj32 pr = project_f32<MATH, SMEM, RK_ICP_ELEV_ONLY ? PROJ_NO_R : PROJ_EXACT>(s, tb, mx, my, mz);
   if (pr.status != PROJ_OK) return;
@@ -380,7 +397,8 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
     q = make_float4(__fadd_rn(__fmul_rn(n.w, d.x), o.x), __fadd_rn(__fmul_rn(n.w, d.y), o.y),
                     __fadd_rn(__fmul_rn(n.w, d.z), o.z), 0.f);
   }
-  accumulate_point<STATS, FUSED>(mx, my, mz, n, q, gate2, inv_k, acc, cost, sumsq, cnt);
+  accumulate_point<STATS, FUSED, MATH != MATH_FAST>(mx, my, mz, n, q, gate2, inv_k, k32, acc, cost,
+                                                          sumsq, cnt);
 }
 
 template <int WPP, int NT>
@@ -466,6 +484,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
     const float gate32 = (float)(A.cfg.max_dist * level);
     const float gate2 = __fmul_rn(gate32, gate32);
     const float inv_k = (float)(1.0 / kern);
+    const float k32 = (float)kern;  // np.float32(kernel_scale) (registration.py:350)
     const float inv_s = (float)(1.0 / stride);
     const int Hs = (H + stride - 1) / stride, Ws = (W + stride - 1) / stride;
     const int npix = Hs * Ws;
@@ -483,7 +502,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
     const int row_step = stride * W;
     if (RK_ICP_LVL_SMEM && gtid == 0) {
       sh_lvl[g][0] = make_float4(gate2, inv_k, inv_s, __int_as_float(stride));
-      sh_lvl[g][1] = make_float4(__int_as_float(lvl_off), __int_as_float(lvl_w), 0.f, 0.f);
+      sh_lvl[g][1] = make_float4(__int_as_float(lvl_off), __int_as_float(lvl_w), k32, 0.f);
       sh_surf[g] = surf;
     }
     // executed work (the roofline's unit) = valid points of this level x the
@@ -544,10 +563,10 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
               const float4 L0 = sh_lvl[g][0], L1 = sh_lvl[g][1];
               associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, sh_surf[g], rec, __float_as_int(L0.w),
                                                  __float_as_int(L1.x), __float_as_int(L1.y), L0.z, L0.x,
-                                                 L0.y, acc, cost, sumsq, cnt);
+                                                 L0.y, L1.z, acc, cost, sumsq, cnt);
             } else {
               associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, stride, lvl_off, lvl_w, inv_s,
-                                                 gate2, inv_k, acc, cost, sumsq, cnt);
+                                                 gate2, inv_k, k32, acc, cost, sumsq, cnt);
             }
           }
         }
@@ -565,9 +584,9 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           float mx, my, mz;
           move_f32(P, r, d4, __ldg(s.origins32 + u), mx, my, mz);
           associate_moved<MATH, SMEM, STATS>(s, tb, mx, my, mz, surf, rec, stride, lvl_off, lvl_w, inv_s,
-                                             gate2, inv_k, acc, cost, sumsq, cnt);
+                                             gate2, inv_k, k32, acc, cost, sumsq, cnt);
         }
-      } else if (col_mode) {
+      } else if (col_mode && RK_ICP_F64_AHEAD) {
         // column-owner walk (Ws % GT == 0): each lane owns view columns
         // gtid, gtid + GT, ... and walks them down the rows with a constant
         // pointer step; the receiver origin depends on the column only
@@ -590,7 +609,30 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
             }
             if (!range_ok(r, cmin, cmax)) continue;
             associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
-                                               lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
+                                               lvl_w, inv_s, gate2, inv_k, k32, acc, cost, sumsq, cnt);
+          }
+        }
+      } else if (col_mode) {
+        // the same walk with the float64 ray and receiver origin loaded at
+        // use (L1 hits) instead of held in registers a row ahead: under the
+        // 64-register cap the held float64 values spill
+        for (int cj = wtid; cj < Ws; cj += WGT) {
+          const int u = cj * stride;
+          const float* sp = src + u;
+          const double* dp = s.dirs + 3 * (size_t)u;
+          float r_next = __ldg(sp);
+          for (int vi = 0; vi < Hs; ++vi) {
+            const float r = r_next;
+            const double* dcp = dp;
+            sp += row_step;
+            dp += 3 * (size_t)row_step;
+            if (vi + 1 < Hs) r_next = __ldg(sp);
+            if (!range_ok(r, cmin, cmax)) continue;
+            const double3 dcur = make_double3(__ldg(dcp), __ldg(dcp + 1), __ldg(dcp + 2));
+            const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
+                                              __ldg(s.origins + 3 * u + 2));
+            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
+                                               lvl_w, inv_s, gate2, inv_k, k32, acc, cost, sumsq, cnt);
           }
         }
       } else {
@@ -619,7 +661,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           const double3 ocur = make_double3(__ldg(s.origins + 3 * u), __ldg(s.origins + 3 * u + 1),
                                             __ldg(s.origins + 3 * u + 2));
           associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
-                                             lvl_w, inv_s, gate2, inv_k, acc, cost, sumsq, cnt);
+                                             lvl_w, inv_s, gate2, inv_k, k32, acc, cost, sumsq, cnt);
         }
       }
       // ---- deterministic group reduction in float64
@@ -805,6 +847,8 @@ int max_active_clusters() {
     cudaLaunchAttribute at[1];
     cudaLaunchConfig_t lc = cluster_config<CL>(1, nullptr, at);
     int n = 0;
+    // (occupancy of the FAST instantiation; the MATH_NP one has the same
+    // 1024-thread CTAs and register cap, so the same clusters fit)
     if (cudaOccupancyMaxActiveClusters(&n, k_register<MATH_FAST, kWide / 32, 1, true, false, kWide, CL>, &lc) !=
             cudaSuccess || n < 1) {
       cudaGetLastError();
@@ -815,7 +859,7 @@ int max_active_clusters() {
   return cache[dev];
 }
 
-template <int CL, int NT = kWide>
+template <int MATH, int CL, int NT = kWide>
 int launch_cluster(const IcpArgs& a, cudaStream_t st) {
   constexpr int WPP = NT / 32;
   const bool smem = a.s.H <= kMaxRowsSmem && a.s.K <= kMaxInvSmem;
@@ -823,11 +867,11 @@ int launch_cluster(const IcpArgs& a, cudaStream_t st) {
   cudaLaunchConfig_t lc = cluster_config<CL, NT>(a.batch, st, at);
   cudaError_t e;
   if (a.stats)
-    e = smem ? cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, true, true, NT, CL>, a)
-             : cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, false, true, NT, CL>, a);
+    e = smem ? cudaLaunchKernelEx(&lc, k_register<MATH, WPP, 1, true, true, NT, CL>, a)
+             : cudaLaunchKernelEx(&lc, k_register<MATH, WPP, 1, false, true, NT, CL>, a);
   else
-    e = smem ? cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, true, false, NT, CL>, a)
-             : cudaLaunchKernelEx(&lc, k_register<MATH_FAST, WPP, 1, false, false, NT, CL>, a);
+    e = smem ? cudaLaunchKernelEx(&lc, k_register<MATH, WPP, 1, true, false, NT, CL>, a)
+             : cudaLaunchKernelEx(&lc, k_register<MATH, WPP, 1, false, false, NT, CL>, a);
   if (e != cudaSuccess) return rk_cuda_status(e, "k_register (cluster)");
   RK_LAUNCHED("k_register");
   return RK_OK;
@@ -844,6 +888,55 @@ int sm_count() {
     cache[dev] = n > 0 ? n : 148;
   }
   return cache[dev];
+}
+
+// tier selection by batch size (the latency modes for batches that cannot
+// fill the GPU with 256-thread CTAs)
+template <int MATH>
+int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) {
+  constexpr int MINB = MATH == MATH_FAST ? RK_ICP_MINB : RK_ICP_MINB_NP;
+  constexpr int WFULL = kThreads / 32;
+  const int batch = a.batch;
+  // latency mode: a batch that cannot fill the GPU with 256-thread CTAs
+  // (online odometry, one register() call, a short sequence) runs each pair
+  // on a 1024-thread CTA (<= one pair per SM) or a 512-thread CTA (<= two):
+  // more warps per pair to hide the gather latency
+  const char* wide = getenv("RK_ICP_WIDE");
+  const char* fnt = getenv("RK_ICP_NT");  // experiment knob: force the CTA size
+  if (!force && fnt) {
+    const int nt = atoi(fnt);
+    if (nt == 1024) return launch<MATH, kWide / 32, 1, kWide>(a, st);
+    if (nt == 512) return launch<MATH, kWide / 64, 2, kWide / 2>(a, st);
+  }
+  if (!force && (!wide || atoi(wide))) {
+    // a few pairs: a cluster of CTAs per pair (RK_ICP_CLUSTER=0 disables,
+    // =2|4|8 forces the size)
+    const char* fcl = getenv("RK_ICP_CLUSTER");
+    const int want = fcl ? atoi(fcl) : -1;
+    if (want != 0) {
+      // the largest cluster whose batch fits in one wave of co-resident
+      // clusters (B200: 1-8 pairs x8, then x4, then <= 74 x2; DESIGN §3)
+      const int cl = want > 0 ? want
+                              : (batch <= max_active_clusters<8>()   ? 8
+                                 : batch <= max_active_clusters<4>() ? 4
+                                 : batch <= max_active_clusters<2>() ? 2
+                                                                     : 1);
+      if (cl == 8) return launch_cluster<MATH, 8>(a, st);
+      if (cl == 4) return launch_cluster<MATH, 4>(a, st);
+      if (cl == 2) return launch_cluster<MATH, 2>(a, st);
+    }
+    if (batch <= sm_count()) return launch<MATH, kWide / 32, 1, kWide>(a, st);
+    if (batch <= 2 * sm_count()) return launch<MATH, kWide / 64, 2, kWide / 2>(a, st);
+  }
+  if constexpr (MATH == MATH_FAST) {  // experiment layouts (RK_ICP_WPP), FAST only
+    switch (wpp) {
+      case 1: return launch<MATH, 1, MINB>(a, st);
+      case 2: return launch<MATH, 2, MINB>(a, st);
+      case 4: return launch<MATH, 4, MINB>(a, st);
+      default: break;
+    }
+  }
+  return launch<MATH, WFULL, MINB>(a, st);
 }
 
 }  // namespace
@@ -890,43 +983,9 @@ extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, con
   cudaStream_t st = S(stream);
   constexpr int MINB = RK_ICP_MINB;
   constexpr int WFULL = kThreads / 32;
+  (void)wpp;
   if (cfg->math == MATH_CR)
     return wpp == 1 ? launch<MATH_CR, 1, MINB>(a, st) : launch<MATH_CR, WFULL, MINB>(a, st);
-  // latency mode: a batch that cannot fill the GPU with 256-thread CTAs
-  // (online odometry, one register() call, a short sequence) runs each pair
-  // on a 1024-thread CTA (<= one pair per SM) or a 512-thread CTA (<= two):
-  // more warps per pair to hide the gather latency
-  const char* wide = getenv("RK_ICP_WIDE");
-  const char* fnt = getenv("RK_ICP_NT");  // experiment knob: force the CTA size
-  if (!force && fnt) {
-    const int nt = atoi(fnt);
-    if (nt == 1024) return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
-    if (nt == 512) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
-  }
-  if (!force && (!wide || atoi(wide))) {
-    // a few pairs: a cluster of CTAs per pair (RK_ICP_CLUSTER=0 disables,
-    // =2|4|8 forces the size)
-    const char* fcl = getenv("RK_ICP_CLUSTER");
-    const int want = fcl ? atoi(fcl) : -1;
-    if (want != 0) {
-      // the largest cluster whose batch fits in one wave of co-resident
-      // clusters (B200: 1-8 pairs x8, then x4, then <= 74 x2; DESIGN §3)
-      const int cl = want > 0 ? want
-                              : (batch <= max_active_clusters<8>()   ? 8
-                                 : batch <= max_active_clusters<4>() ? 4
-                                 : batch <= max_active_clusters<2>() ? 2
-                                                                     : 1);
-      if (cl == 8) return launch_cluster<8>(a, st);
-      if (cl == 4) return launch_cluster<4>(a, st);
-      if (cl == 2) return launch_cluster<2>(a, st);
-    }
-    if (batch <= sm_count()) return launch<MATH_FAST, kWide / 32, 1, kWide>(a, st);
-    if (batch <= 2 * sm_count()) return launch<MATH_FAST, kWide / 64, 2, kWide / 2>(a, st);
-  }
-  switch (wpp) {
-    case 1: return launch<MATH_FAST, 1, MINB>(a, st);
-    case 2: return launch<MATH_FAST, 2, MINB>(a, st);
-    case 4: return launch<MATH_FAST, 4, MINB>(a, st);
-    default: return launch<MATH_FAST, WFULL, MINB>(a, st);
-  }
+  if (cfg->math == MATH_NP) return launch_tiers<MATH_NP>(a, st, force, wpp);
+  return launch_tiers<MATH_FAST>(a, st, force, wpp);
 }

@@ -41,6 +41,12 @@ static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p)
 static inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 // ------------------------------------------------------------------ sensor
+// VRSQRT14PS table for MATH_NP's arcsin (rk_svml.cuh); generated at build time
+// from data/vrsqrt14.u16 (scripts/gen_vrsqrt14.c) by __graft_entry__.build()
+static const uint16_t kVrsqrt14[65536] = {
+#include "rk_vrsqrt14.inc"
+};
+
 extern "C" int rk_sensor_create(const rk_sensor_desc* d, rk_sensor** out) {
   if (!d || !out) { rk_set_error("null argument"); return RK_EGENERIC; }
   const int H = d->height, W = d->width, K = d->inv_size;
@@ -58,6 +64,7 @@ extern "C" int rk_sensor_create(const rk_sensor_desc* d, rk_sensor** out) {
   size_t o_az = take(H * sizeof(double));
   size_t o_el = take(H * sizeof(double));
   size_t o_inv = take(K * sizeof(int32_t));
+  size_t o_rs14 = take(sizeof(kVrsqrt14));
   std::vector<unsigned char> host(off, 0);
   memcpy(&host[o_dirs], d->dirs_host, HW * 3 * sizeof(double));
   memcpy(&host[o_orig], d->origins_host, (size_t)W * 3 * sizeof(double));
@@ -75,6 +82,7 @@ extern "C" int rk_sensor_create(const rk_sensor_desc* d, rk_sensor** out) {
   memcpy(&host[o_az], d->azimuth_host, H * sizeof(double));
   memcpy(&host[o_el], d->elevation_host, H * sizeof(double));
   memcpy(&host[o_inv], d->inv_rows_host, K * sizeof(int32_t));
+  memcpy(&host[o_rs14], kVrsqrt14, sizeof(kVrsqrt14));
 
   rk_sensor* s = new rk_sensor();
   cudaGetDevice(&s->device);
@@ -95,6 +103,7 @@ extern "C" int rk_sensor_create(const rk_sensor_desc* d, rk_sensor** out) {
   v.az = reinterpret_cast<const double*>(b + o_az);
   v.el = reinterpret_cast<const double*>(b + o_el);
   v.inv_rows = reinterpret_cast<const int32_t*>(b + o_inv);
+  v.rsqrt14 = reinterpret_cast<const uint16_t*>(b + o_rs14);
   v.K = K;
   v.inv_lo = d->inv_phi_min;
   v.inv_scale = (double)(K - 1) / (d->inv_phi_max - d->inv_phi_min);
@@ -131,6 +140,24 @@ __global__ void k_project_f32(SensorDev s, const float* __restrict__ pts, int64_
   }
 }
 
+__global__ void k_svml_eval(SensorDev s, int fn, const float* __restrict__ a, const float* __restrict__ b,
+                            int64_t n, float* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fn == 0 ? svml_atan2f(a[i], b[i]) : svml_asinf(a[i], s.rsqrt14);
+}
+
+extern "C" int rk_svml_eval(const rk_sensor* s, int fn, const float* a, const float* b, int64_t n,
+                            float* out, void* stream) {
+  if (n <= 0) return RK_OK;
+  if (fn != 0 && fn != 1) { rk_set_error("fn must be 0 (arctan2) or 1 (arcsin)"); return RK_EGENERIC; }
+  if (fn == 0 && !b) { rk_set_error("arctan2 needs b"); return RK_EGENERIC; }
+  unsigned g = min(blocks_for(n, 256), 148u * 16u);
+  k_svml_eval<<<g, 256, 0, S(stream)>>>(s->dev, fn, a, b, n, out);
+  RK_LAUNCHED("k_svml_eval");
+  return RK_OK;
+}
+
 extern "C" int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, int math,
                               float* u, int32_t* v, float* r, int8_t* status, void* stream) {
   if (n <= 0) return RK_OK;
@@ -139,6 +166,8 @@ extern "C" int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, i
     k_project_f32<MATH_CR><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   else if (math == MATH_LIBM)
     k_project_f32<MATH_LIBM><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
+  else if (math == MATH_NP)
+    k_project_f32<MATH_NP><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   else
     k_project_f32<MATH_FAST><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   RK_LAUNCHED("k_project_f32");

@@ -430,8 +430,8 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
 #endif
         const float wn = __fadd_rn(st.y, 1.0f);
         // (w*tsdf + d) / (w + 1), correctly rounded (w + 1 in [1, max_weight + 1])
-        st.x = MATH == MATH_FAST ? div_rn_fast(__fadd_rn(__fmul_rn(st.y, st.x), d), wn)
-                                 : __fdiv_rn(__fadd_rn(__fmul_rn(st.y, st.x), d), wn);
+        st.x = MATH != MATH_CR ? div_rn_fast(__fadd_rn(__fmul_rn(st.y, st.x), d), wn)
+                               : __fdiv_rn(__fadd_rn(__fmul_rn(st.y, st.x), d), wn);
         st.y = fminf(wn, A.max_w);
         vox[i] = st;
         ++count;
@@ -612,10 +612,12 @@ static cudaError_t set_integrate_attrs() {
   (void)num_sms();  // cached now: rk_grid_integrate may later run under graph capture
   const int smem = (int)kLatticeBytes;
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_integrate<MATH_CR, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_integrate<MATH_CR, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  return cudaFuncSetAttribute(k_integrate<MATH_FAST, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const void* fns[] = {(const void*)k_integrate<MATH_CR, NT, true>, (const void*)k_integrate<MATH_CR, NT, false>,
+                       (const void*)k_integrate<MATH_FAST, NT, true>, (const void*)k_integrate<MATH_FAST, NT, false>,
+                       (const void*)k_integrate<MATH_NP, NT, true>, (const void*)k_integrate<MATH_NP, NT, false>};
+  for (const void* f : fns)
+    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  return cudaSuccess;
 }
 
 struct rk_grid {
@@ -876,6 +878,9 @@ static int integrate_slot(rk_grid* g, const rk_sensor* s, const float* range, co
   if (math == MATH_CR)
     tab ? k_integrate<MATH_CR, NT, true><<<grid, NT, smem, st>>>(a)
         : k_integrate<MATH_CR, NT, false><<<grid, NT, smem, st>>>(a);
+  else if (math == MATH_NP)
+    tab ? k_integrate<MATH_NP, NT, true><<<grid, NT, smem, st>>>(a)
+        : k_integrate<MATH_NP, NT, false><<<grid, NT, smem, st>>>(a);
   else
     tab ? k_integrate<MATH_FAST, NT, true><<<grid, NT, smem, st>>>(a)
         : k_integrate<MATH_FAST, NT, false><<<grid, NT, smem, st>>>(a);

@@ -31,9 +31,11 @@ PROJ_OK = 0
 PROJ_OUT_OF_FOV = 1
 PROJ_DEGENERATE = 2
 
-MATH_FAST = 0   # minimax atan2 / asin (<= 2.5 ulp) + refined reciprocals (default)
+MATH_FAST = 0   # minimax atan2 / asin (<= 2.5 ulp) + refined reciprocals, float32 ICP move
 MATH_CR = 1     # float64-evaluated, rounded once (parity mode)
 MATH_LIBM = 2   # CUDA atan2f / asinf (<= 2 ulp), IEEE division (project_many only)
+MATH_NP = 3     # numpy's own float32 arctan2 / arcsin (SVML, rk_svml.cuh), float64 ICP move:
+                # the reference's projection bit for bit
 
 _default_math = MATH_FAST
 
