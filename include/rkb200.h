@@ -82,9 +82,10 @@ int rk_sensor_destroy(rk_sensor* s);
 /* project_many(single=True, refine=False)  lidar_model.py:262-344 */
 int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, int math,
                    float* u, int32_t* v, float* r, int8_t* status, void* stream);
-/* diagnostic: RK_MATH_NP's transcendentals elementwise on device arrays --
+/* diagnostic: RK_MATH_NP's arithmetic elementwise on device arrays --
  * fn 0: out = np.arctan2(a, b) (lidar_model.py:288), fn 1: out = np.arcsin(a)
- * (lidar_model.py:45; |a| <= 1), float32 (parity tests against numpy) */
+ * (lidar_model.py:45; |a| <= 1), fn 2: the kernels' range-check-free
+ * division a / b, fn 3: IEEE a / b; float32 (parity tests) */
 int rk_svml_eval(const rk_sensor* s, int fn, const float* a, const float* b, int64_t n,
                  float* out, void* stream);
 /* project_many(single=False) float64 fixed-point path, lidar_model.py:287-344.

@@ -27,7 +27,7 @@
 using namespace rk;
 
 #ifndef RK_ICP_MINB_NP  // CTAs per SM for the numpy-exact kernel
-#define RK_ICP_MINB_NP 4
+#define RK_ICP_MINB_NP 3  // 85 registers: the exact float64 walk spills at 64 (A/B: +7%)
 #endif
 #ifndef RK_ICP_MINB
 #define RK_ICP_MINB 4
@@ -249,10 +249,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 // roundings, so MATH_CR associates exactly like the oracle.
 // q: the association target {x, y, z} (registration.py:168-176), from the
 // surfel pyramid record or formed from the ray tables by the caller.
-// EXACT_COST (the exact modes): the IterationStats cost term is the
-// reference's own expression 1/w - 1 with w = 1 / sqrt(1 + (r/k)^2) in
-// float32 (registration.py:350-352, 357-358), cancellation included.
-template <bool STATS, bool FUSED = false, bool EXACT_COST = false>
+// EXACT (the exact modes): the IRLS weight is the reference's own float32
+// expression w = 1 / sqrt(1 + (r/k)^2) (robust_weight32, registration.py:
+// 357-358; IEEE division and square root), so every per-point term equals
+// the reference's and only the summation order differs; the IterationStats
+// cost term is its 1/w - 1 (registration.py:352), cancellation included.
+template <bool STATS, bool FUSED = false, bool EXACT = false>
 __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, const float4& n,
                                                  const float4& q, float gate2, float inv_k, float k32,
                                                  float* acc, float& cost, float& sumsq, int& cnt) {
@@ -286,9 +288,16 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   J[3] = n.x;
   J[4] = n.y;
   J[5] = n.z;
-  const float e = res * inv_k;
-  const float s1 = __fmaf_rn(e, e, 1.0f);
-  const float w = rsqrtf(s1);
+  float e, s1, w;
+  if (EXACT) {
+    e = div_rn_fast(res, k32);
+    s1 = __fadd_rn(1.0f, __fmul_rn(e, e));
+    w = div_rn_fast(1.0f, __fsqrt_rn(s1));
+  } else {
+    e = res * inv_k;
+    s1 = __fmaf_rn(e, e, 1.0f);
+    w = rsqrtf(s1);
+  }
   const float rw = -res * w;
   int h = 0;
 #pragma unroll
@@ -300,10 +309,8 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
 #pragma unroll
   for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
   if (STATS) {
-    if (EXACT_COST) {
-      const float ek = __fdiv_rn(res, k32);
-      const float wx = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(1.0f, __fmul_rn(ek, ek))));
-      cost = __fadd_rn(cost, __fsub_rn(__fdiv_rn(1.0f, wx), 1.0f));
+    if (EXACT) {
+      cost = __fadd_rn(cost, __fsub_rn(div_rn_fast(1.0f, w), 1.0f));
     } else {
       // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
       cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));

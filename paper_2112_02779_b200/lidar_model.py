@@ -31,23 +31,44 @@ PROJ_OK = 0
 PROJ_OUT_OF_FOV = 1
 PROJ_DEGENERATE = 2
 
-MATH_FAST = 0   # minimax atan2 / asin (<= 2.5 ulp) + refined reciprocals, float32 ICP move
+MATH_FAST = 0   # minimax atan2 / asin (<= 2.5 ulp) + MUFU square roots, float32 ICP move
 MATH_CR = 1     # float64-evaluated, rounded once (parity mode)
 MATH_LIBM = 2   # CUDA atan2f / asinf (<= 2 ulp), IEEE division (project_many only)
 MATH_NP = 3     # numpy's own float32 arctan2 / arcsin (SVML, rk_svml.cuh), float64 ICP move:
-                # the reference's projection bit for bit
+                # the reference's projection bit for bit (default)
 
-_default_math = MATH_FAST
+_default_math = MATH_NP
 
 
 def set_default_math(mode: int) -> None:
-    """Select the float32 transcendental mode used by every bulk kernel."""
+    """Select the projection arithmetic of every bulk kernel: MATH_NP (default,
+    the reference's own bits), MATH_FAST (faster, within the tolerance
+    contract), MATH_CR (correctly rounded transcendentals)."""
     global _default_math
+    if int(mode) not in (MATH_FAST, MATH_CR, MATH_LIBM, MATH_NP):
+        raise ValueError(f"unknown math mode {mode}")
     _default_math = int(mode)
 
 
 def default_math() -> int:
     return _default_math
+
+
+class math_mode:
+    """``with math_mode(MATH_FAST): ...`` -- the default mode inside the block,
+    restored on exit."""
+
+    def __init__(self, mode: int):
+        self.mode = int(mode)
+
+    def __enter__(self):
+        self.prev = default_math()
+        set_default_math(self.mode)
+        return self
+
+    def __exit__(self, *exc):
+        set_default_math(self.prev)
+        return False
 
 
 def round_half_up(x):

@@ -69,7 +69,11 @@ def launches(tag, path):
 
 
 def full(tag, rep):
-    rows = ncu_csv(["-i", str(rep), "--page", "raw"])
+    rep = Path(rep)
+    if rep.suffix == ".csv":   # the raw page exported on the GPU box (gpu_ncu.sh)
+        rows = list(csv.reader(open(rep)))
+    else:
+        rows = ncu_csv(["-i", str(rep), "--page", "raw"])
     h, units = rows[0], rows[1]
     col = {n: i for i, n in enumerate(h)}
     out = [f"# {tag}: ncu --set full captures", "", f"Source: `{Path(rep).name}` (not committed; "
@@ -116,9 +120,10 @@ def main():
     lp = Path(a.launches or ROOT / "gpurun_out" / f"launches_{a.tag}.csv")
     if lp.exists():
         launches(a.tag, lp)
-    reps = [Path(a.rep)] if a.rep else sorted((ROOT / "gpurun_out").glob(f"prof_*{a.tag}.ncu-rep"))
+    reps = [Path(a.rep)] if a.rep else (sorted((ROOT / "gpurun_out").glob(f"prof_*{a.tag}.ncu-rep"))
+                                         or sorted((ROOT / "gpurun_out").glob(f"raw_*_{a.tag}.csv")))
     for rp in reps:
-        name = rp.stem.replace("prof_", "").replace(f"_{a.tag}", "")
+        name = rp.stem.replace("prof_", "").replace("raw_", "").replace(f"_{a.tag}", "")
         full(a.tag if name == a.tag else f"{a.tag}_{name}", rp)
 
 

@@ -78,3 +78,12 @@ def sensors():
 def osensors(sensors):
     from oracle.sensor import Sensor
     return {k: Sensor.from_intrinsics(v) for k, v in sensors.items()}
+
+
+@pytest.fixture
+def fast_math():
+    """Run a test in MATH_FAST (the opt-in tolerance-contract mode; the
+    default MATH_NP has its own bit-exact tests, test_gpu_numpy_exact.py)."""
+    from paper_2112_02779_b200 import lidar_model as lm
+    with lm.math_mode(lm.MATH_FAST):
+        yield

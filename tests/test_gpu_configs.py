@@ -55,11 +55,8 @@ def test_register_cr_vs_oracle(rk, case):
     name, intr, S, src, dst, gt = case
     vec, valid = oimg.normals_cross(S, dst)
     ref = oicp.register(S, src, dst, vec, valid, math="cr", fma="exact")
-    lm.set_default_math(lm.MATH_CR)
-    try:
+    with lm.math_mode(lm.MATH_CR):
         res = rk.register(rk.RangeImage(src, intr), rk.RangeImage(dst, intr))
-    finally:
-        lm.set_default_math(lm.MATH_FAST)
     assert res.converged == ref["converged"]
     assert np.abs(res.pose.R - ref["R"]).max() < 1e-6 and np.abs(res.pose.t - ref["t"]).max() < 1e-6
     assert [(s.stride, s.iteration) for s in res.stats] == [(int(s[0]), int(s[1])) for s in ref["stats"]]
@@ -79,11 +76,8 @@ def test_tsdf_frame_cr_bitexact(rk, case):
     keys, n_ref = otsdf.integrate_cloud_frame(og, S, dst, gt.R, gt.t, voxel, 4 * voxel,
                                               clip_max=30.0, math="cr")
     grid = rk.VoxelBlockGrid(voxel_size=voxel)
-    lm.set_default_math(lm.MATH_CR)
-    try:
+    with lm.math_mode(lm.MATH_CR):
         n = rk.integrate_cloud_frame(grid, rk.RangeImage(dst, intr), gt, clip_max=30.0)
-    finally:
-        lm.set_default_math(lm.MATH_FAST)
     assert n == n_ref
     k, vox = grid.export_blocks()
     assert [tuple(x) for x in k.tolist()] == sorted(og)
@@ -102,12 +96,9 @@ def test_mesh_c3_vs_oracle(rk):
     otsdf.integrate_cloud_frame(og, S, dst, np.eye(3), np.zeros(3), 0.1, 0.4, clip_max=30.0, math="cr")
     V, T, N = omesh.extract_mesh(og, 0.1)
     grid = rk.VoxelBlockGrid(voxel_size=0.1)
-    lm.set_default_math(lm.MATH_CR)
-    try:
+    with lm.math_mode(lm.MATH_CR):
         rk.integrate_cloud_frame(grid, rk.RangeImage(dst, intr), rk.RigidTransform.identity(),
                                  clip_max=30.0)
-    finally:
-        lm.set_default_math(lm.MATH_FAST)
     m = rk.extract_mesh(grid)
     assert m.n_vertices == V.shape[0] and m.n_triangles == T.shape[0] > 1000
     pos = {tuple(p): i for i, p in enumerate(V.tolist())}

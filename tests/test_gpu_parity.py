@@ -6,10 +6,12 @@ Contract (BASELINE.json north_star):
   normals, voxel-block allocation; with RK_MATH_CR (float64-evaluated
   transcendentals in both kernel and oracle) also projection, association
   sets and TSDF values;
-* with the product math (RK_MATH_FAST: minimax atan2/asin, refined
-  reciprocals, vs numpy's SVML): >= 99.9 % correspondence-mask agreement,
-  poses within 1e-5 rad / 1e-5 m with equal iteration counts, TSDF values
-  within 1e-5.
+* with the opt-in RK_MATH_FAST (minimax atan2/asin, MUFU square roots,
+  float32 ICP move, vs numpy's SVML): >= 99.9 % correspondence-mask
+  agreement, poses within 1e-5 rad / 1e-5 m with equal iteration counts,
+  TSDF values within 1e-5 (the "*_vs_reference" tests that use the
+  fast_math fixture).  The default RK_MATH_NP is bit-exact against the
+  reference: tests/test_gpu_numpy_exact.py.
 """
 
 import numpy as np
@@ -89,6 +91,7 @@ def test_project_f32_cr_bitexact_vs_oracle(rk, name, sensors, osensors, golden_p
     assert np.array_equal(r, orr)
 
 
+@pytest.mark.usefixtures("fast_math")
 @pytest.mark.parametrize("name", ("small", "synth", "ouster"))
 def test_project_f32_fast_vs_reference(rk, name, sensors, golden_proj):
     g = golden_proj
@@ -179,8 +182,7 @@ def test_correspondences_cr_bitexact_vs_oracle(rk, pair, sensors, osensors, gold
     src_pts = _src_cloud(rk, pair, sensors, golden_icp)
     M = g[f"{pair}/corr_pose"]
     pose = rk.RigidTransform(M[:3, :3], M[:3, 3])
-    lm.set_default_math(lm.MATH_CR)
-    try:
+    with lm.math_mode(lm.MATH_CR):
         for s in (1, 2, 4):
             c = rk.projective_correspondences(src_pts, dst, nm, pose, 0.5 * s, s, single=True)
             sel, tgt, nrm, _ = oicp.correspondences_f32(osensors[SENSOR_OF[pair]], src_pts, g[f"{pair}/dst"],
@@ -188,10 +190,9 @@ def test_correspondences_cr_bitexact_vs_oracle(rk, pair, sensors, osensors, gold
                                                         M[:3, 3], 0.5 * s, s, math="cr")
             assert np.array_equal(c.source, src_pts[sel])
             assert np.array_equal(c.target, tgt) and np.array_equal(c.normal, nrm)
-    finally:
-        lm.set_default_math(lm.MATH_FAST)
 
 
+@pytest.mark.usefixtures("fast_math")
 @pytest.mark.parametrize("pair", PAIRS)
 def test_correspondence_masks_vs_reference(rk, pair, sensors, golden_icp):
     g, intr = golden_icp, sensors[SENSOR_OF[pair]]
@@ -216,6 +217,7 @@ def test_correspondence_masks_vs_reference(rk, pair, sensors, golden_icp):
 
 # ---------------------------------------------------------------- registration (K3)
 
+@pytest.mark.usefixtures("fast_math")
 @pytest.mark.parametrize("pair", PAIRS)
 def test_register_vs_reference(rk, pair, sensors, golden_icp):
     g, intr = golden_icp, sensors[SENSOR_OF[pair]]
@@ -240,11 +242,8 @@ def test_register_cr_vs_oracle(rk, pair, sensors, osensors, golden_icp):
     from paper_2112_02779_b200 import lidar_model as lm
     g, intr = golden_icp, sensors[SENSOR_OF[pair]]
     src, dst = rk.RangeImage(g[f"{pair}/src"], intr), rk.RangeImage(g[f"{pair}/dst"], intr)
-    lm.set_default_math(lm.MATH_CR)
-    try:
+    with lm.math_mode(lm.MATH_CR):
         res = rk.register(src, dst)
-    finally:
-        lm.set_default_math(lm.MATH_FAST)
     ref = oicp.register(osensors[SENSOR_OF[pair]], g[f"{pair}/src"], g[f"{pair}/dst"], g[f"{pair}/nrm"],
                         g[f"{pair}/nvalid"], math="cr")
     assert res.converged == ref["converged"]
@@ -470,11 +469,8 @@ def test_tsdf_sequence_cr_bitexact_vs_oracle(rk, sensors, osensors, golden_tsdf)
     from oracle import tsdf as otsdf
     from paper_2112_02779_b200 import lidar_model as lm
     g = golden_tsdf
-    lm.set_default_math(lm.MATH_CR)
-    try:
+    with lm.math_mode(lm.MATH_CR):
         grid, counts = _seq_grid(rk, sensors, g)
-    finally:
-        lm.set_default_math(lm.MATH_FAST)
     og, oc = {}, []
     for f, M in zip(g["seq_frames"], g["seq_poses"]):
         oc.append(otsdf.integrate_cloud_frame(og, osensors["small"], f, M[:3, :3], M[:3, 3], 0.2, 0.8,
@@ -486,6 +482,7 @@ def test_tsdf_sequence_cr_bitexact_vs_oracle(rk, sensors, osensors, golden_tsdf)
     assert np.array_equal(vox, ovox)
 
 
+@pytest.mark.usefixtures("fast_math")
 def test_tsdf_sequence_vs_reference(rk, sensors, golden_tsdf):
     g = golden_tsdf
     grid, counts = _seq_grid(rk, sensors, g)
@@ -500,6 +497,7 @@ def test_tsdf_sequence_vs_reference(rk, sensors, golden_tsdf):
     assert np.mean(ok == g["q_ok"]) >= 0.99
 
 
+@pytest.mark.usefixtures("fast_math")
 def test_tsdf_street_frame_vs_reference(rk, sensors, golden_tsdf, golden_icp):
     g = golden_tsdf
     grid = rk.VoxelBlockGrid(voxel_size=0.05)
