@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--frames", type=int, default=100)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the extra one-GPU lines (math modes, K1 per pair, independent-pair e2e, "
+                         "C5 TSDF, per-kernel rooflines)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     # TSDF sequence shape: c2 (default; 64x1024 Ouster-like, 5 cm), c3 (HDL-64
     # 64x2048, 10 cm), c5 (OS-128 128x2048, 3 cm) -- BASELINE.json configs
@@ -446,6 +449,240 @@ def run_e2e(args, rank, world, dist, D, tsdf, cfg):
                      "are read on the host after step k+1 is enqueued")
 
 
+# ------------------------------------------------------------------ extra lines (one GPU)
+
+def _events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def run_math_modes(args, D, cfg, modes=("fast", "cr")):
+    """The same ICP + TSDF step in the other projection-arithmetic modes
+    (MATH_NP is the headline): registrations/s and TSDF frames/s, one warm-up
+    and two timed repetitions each, CUDA events."""
+    import torch
+
+    import paper_2112_02779_b200 as rk
+    from paper_2112_02779_b200 import lidar_model as lm, pipeline
+    from paper_2112_02779_b200.range_image import normals_cross_batch
+    intr = D["intr"]
+    out = {}
+    grid = rk.VoxelBlockGrid(voxel_size=TSDF_VOXEL[args.tsdf_config], capacity=TSDF_CAPACITY[args.tsdf_config])
+    for name in modes:
+        mode = {"fast": lm.MATH_FAST, "cr": lm.MATH_CR, "np": lm.MATH_NP}[name]
+        with lm.math_mode(mode):
+            pt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            upd = torch.zeros(1, dtype=torch.int64, device="cuda")
+            ms_icp = ms_tsdf = 0.0
+            for rep in range(3):
+                a, b = _events()
+                c, d = _events()
+                a.record()
+                surf = normals_cross_batch(intr, D["dst"], strides=[s for s, _ in cfg.schedule])
+                rk.register_batch(intr, D["src"], D["dst"], surf, pair_src=D["pair_idx"], pair_dst=D["pair_dst"],
+                                  config=cfg, pt_iters=pt if rep else None)
+                b.record()
+                pipeline.clear_grid(grid)
+                c.record()
+                pipeline.integrate_sequence(grid, D["tintr"], D["frames"], D["poses_w"], D["inv_w"],
+                                            clip_max=30.0, updated=upd, graph=True)
+                d.record()
+                torch.cuda.synchronize()
+                if rep:
+                    ms_icp += a.elapsed_time(b)
+                    ms_tsdf += c.elapsed_time(d)
+            out[name] = {"registrations_per_s": D["n_pairs"] * 2 / (ms_icp / 1e3),
+                         "tsdf_frames_per_s": args.frames * 2 / (ms_tsdf / 1e3),
+                         "point_iterations_per_step": pt.item() / 2}
+    return out
+
+
+def run_k1_per_pair(args, D, cfg, icp_kernel_ms):
+    """``value`` with K1 charged per pair: the bench's pool computes the
+    destination normals once per pool image (2,048) and reuses them across
+    the 65,536 pairs; truly independent pairs need one K1 per pair.  K1 over
+    the pool is timed and scaled to one image per pair."""
+    import torch
+
+    from paper_2112_02779_b200.range_image import normals_cross_batch
+    intr = D["intr"]
+    normals_cross_batch(intr, D["dst"], strides=[s for s, _ in cfg.schedule])
+    a, b = _events()
+    a.record()
+    reps = 5
+    for _ in range(reps):
+        normals_cross_batch(intr, D["dst"], strides=[s for s, _ in cfg.schedule])
+    b.record()
+    torch.cuda.synchronize()
+    k1_ms_per_image = a.elapsed_time(b) / reps / D["dst"].shape[0]
+    n = D["n_pairs"]
+    step_ms = icp_kernel_ms + k1_ms_per_image * n
+    H, W = intr.height, intr.width
+    coarse = sum(-(-H // s) * -(-W // s) for s, _ in cfg.schedule if s > 1)
+    k1_bytes = 4 * H * W + 16 * (H * W + coarse)          # range in, surfel pyramid out
+    peak, _ = measured_peak()
+    achieved = k1_bytes / (k1_ms_per_image / 1e3) / 1e9
+    return {"value": n / (step_ms / 1e3), "unit": "registrations/s",
+            "k1_us_per_image": k1_ms_per_image * 1e3, "ms_per_step": step_ms,
+            "what": "C4 with K1 normals computed for every pair's destination (65,536 per step) "
+                    "instead of once per pool image",
+            "k1_roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                            "frac": achieved / peak, "bytes_per_image": k1_bytes}}
+
+
+def run_e2e_independent(args, D, cfg):
+    """End to end for truly independent pairs: every pair's own source and
+    destination images cross PCIe (2 x 256 KB per pair, 34 GB per 65,536-pair
+    step), chunked by the pool size and double-buffered on a copy stream, K1
+    per pair, K3, poses back to the host.  The host images of chunk k are the
+    pool's (same bytes per pair as distinct images would move)."""
+    import torch
+
+    import paper_2112_02779_b200 as rk
+    from paper_2112_02779_b200.range_image import normals_cross_batch
+    intr = D["intr"]
+    P = D["src"].shape[0]
+    n = D["n_pairs"]
+    chunks = max(1, n // P)
+    src_h = D["src"].cpu().pin_memory()
+    dst_h = D["dst"].cpu().pin_memory()
+    bufs = [(torch.empty_like(D["src"]), torch.empty_like(D["dst"])) for _ in range(2)]
+    copy = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    out_h = torch.empty((chunks, P, 12), dtype=torch.float64, pin_memory=True)
+
+    def issue(b):
+        with torch.cuda.stream(copy):
+            copy.wait_event(free[b])
+            bufs[b][0].copy_(src_h, non_blocking=True)
+            bufs[b][1].copy_(dst_h, non_blocking=True)
+            ready[b].record(copy)
+
+    def step():
+        issue(0)
+        for k in range(chunks):
+            b = k % 2
+            if k + 1 < chunks:
+                issue(1 - b)
+            main.wait_event(ready[b])
+            src, dst = bufs[b]
+            surf = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
+            res = rk.register_batch(intr, src, dst, surf, config=cfg)
+            free[b].record(main)
+            out_h[k].copy_(res.poses, non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    t0 = time.perf_counter()
+    reps = 2
+    for _ in range(reps):
+        step()
+    el = (time.perf_counter() - t0) / reps
+    h2d = chunks * P * 2 * intr.height * intr.width * 4
+    return {"value": chunks * P / el, "unit": "registrations/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(chunks * P * 12 * 8), "seconds_per_step": el,
+            "h2d_gbs": h2d / el / 1e9,
+            "what": f"{chunks * P} independent pairs per step: each pair's two images copied H2D "
+                    f"(chunks of {P}, double-buffered), K1 per pair, K3, poses D2H; wall clock"}
+
+
+def run_c5_tsdf(frames: int = 100):
+    """C5's TSDF: OS-128 128x2048 extended street at 0.5 m/frame,
+    3 cm voxels -- the grid (~24k blocks, ~0.8 GB) is far beyond the 126 MB
+    L2, so K5 streams its voxel states from HBM.  One warm-up, two timed
+    sequences into a cleared grid, CUDA events."""
+    import torch
+
+    import paper_2112_02779_b200 as rk
+    from paper_2112_02779_b200 import pipeline, scenes
+    intr = scenes.os128()
+    traj = scenes.street_trajectory(frames, seed=0, step_m=0.5, jitter=0.0002)
+    fr = pipeline.render_batch(intr, scenes.extended_street_scene(0.5 * frames + 30.0), traj)
+    poses_w = torch.from_numpy(pipeline.poses_to_rows(traj)).cuda()
+    inv_w = torch.from_numpy(np.stack([p.inverse().as_row12() for p in traj])).cuda()
+    grid = rk.VoxelBlockGrid(voxel_size=0.03, capacity=TSDF_CAPACITY["c5"])
+    upd = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ms = 0.0
+    for rep in range(3):
+        pipeline.clear_grid(grid)
+        upd.zero_()
+        a, b = _events()
+        a.record()
+        pipeline.integrate_sequence(grid, intr, fr, poses_w, inv_w, clip_max=80.0, updated=upd, graph=True)
+        b.record()
+        torch.cuda.synchronize()
+        if rep:
+            ms += a.elapsed_time(b)
+    ms /= 2
+    n_blocks, _, overflow, _ = grid.info()
+    if overflow:
+        raise RuntimeError("C5 TSDF pool overflow")
+    tsdf_bytes = TSDF_BYTES_PER_VOXEL * upd.item() + TSDF_BYTES_PER_PIXEL * intr.height * intr.width * frames
+    peak, src = measured_peak()
+    achieved = tsdf_bytes / (ms / 1e3) / 1e9
+    return {"value": frames / (ms / 1e3), "unit": "frames/s", "frames": frames, "voxel_m": 0.03,
+            "blocks": int(n_blocks), "grid_bytes": int(n_blocks) * 32768,
+            "voxels_updated_per_frame": upd.item() / frames,
+            "roofline": {"bound": "hbm", "kernel": "k_integrate (+ overlapped k_activate_image)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "work": f"16 B x {upd.item():.4g} updated voxels + 4 B x range pixels, "
+                                 f"{ms:.2f} ms per sequence", "peak_source": src}}
+
+
+def kernel_rooflines(args, D, r, tsdf):
+    """Per-kernel HBM rooflines for the kernels besides K3/K5: K1 (normals +
+    surfel pyramid over the pool), K4 (block activation of the sequence, run
+    alone) and K6 (marching cubes of the final grid, wall clock incl. its one
+    count readback, so an upper bound on kernel time)."""
+    import torch
+
+    from paper_2112_02779_b200 import _native as nat, lidar_model as lm
+    peak, _ = measured_peak()
+    out = {}
+    intr = D["intr"]
+    H, W = intr.height, intr.width
+    cfg_coarse = sum(-(-H // s) * -(-W // s) for s in (4, 2))
+    k1_bytes = D["dst"].shape[0] * (4 * H * W + 16 * (H * W + cfg_coarse))
+    out["k_normals_cross_pyramid"] = {"bound": "hbm", "ms": r["normals_ms"],
+                                      "achieved": k1_bytes / (r["normals_ms"] / 1e3) / 1e9, "peak": peak,
+                                      "unit": "GB/s", "bytes": k1_bytes,
+                                      "what": "4 B range in + 16 B surfel out per pixel (+ coarse levels)"}
+    grid = tsdf.grid
+    g = grid._ensure()
+    F = args.frames
+    tin = D["tintr"]
+    nat.call("rk_grid_reserve_slots", g, F, nat.stream_ptr())
+    grid._graphs.clear()   # the slot tables may have moved: drop recorded sequences
+    for rep in range(2):
+        from paper_2112_02779_b200 import pipeline
+        pipeline.clear_grid(grid)
+        a, b = _events()
+        a.record()
+        nat.call("rk_grid_activate_frames", g, lm.device_sensor(tin), nat.ptr(D["frames"]), F,
+                 nat.ptr(D["poses_w"]), float(grid.truncation), 0.0, 30.0, nat.stream_ptr())
+        b.record()
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    k4_bytes = F * 4 * tin.height * tin.width
+    out["k_activate_image"] = {"bound": "hbm", "ms": ms, "achieved": k4_bytes / (ms / 1e3) / 1e9,
+                               "peak": peak, "unit": "GB/s", "bytes": k4_bytes,
+                               "what": f"{F} frames: 4 B range per pixel (+ hash probes, latency-bound); "
+                                       "overlapped with K5 in the sequence"}
+    m = r["mesh"]
+    if m and "ms" in m:
+        nb = m.get("blocks", 0)
+        mc_bytes = nb * 4096 * 8 * (19 ** 3 / 16 ** 3) + m["vertices"] * 48 + m["triangles"] * 12
+        out["k_mc"] = {"bound": "hbm", "ms": m["ms"], "achieved": mc_bytes / (m["ms"] / 1e3) / 1e9,
+                       "peak": peak, "unit": "GB/s", "bytes": mc_bytes,
+                       "what": "8 B per voxel of the 19^3 halo window per block + 48 B per vertex "
+                               "(position, normal) + 12 B per triangle; wall clock incl. one readback"}
+    for v in out.values():
+        v["frac"] = v["achieved"] / v["peak"]
+    return out
+
+
 # ------------------------------------------------------------------ CPU oracle
 
 def _cpu_icp_job(seed_pairs):
@@ -505,8 +742,7 @@ def cpu_icp_baseline(budget_s: float, steps: int = 1, warmup: int = 0):
                        f"{busy:.1f} s compute ({wall:.1f} s wall)")
 
 
-def cpu_tsdf_baseline(frames: int = 3):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+def cpu_tsdf_baseline(frames: int = 3, threads: int = 1):
     from oracle import sensor as osens
     from oracle import synth as osynth
     from oracle import tsdf as otsdf
@@ -518,10 +754,109 @@ def cpu_tsdf_baseline(frames: int = 3):
     grid = {}
     t0 = time.perf_counter()
     for img, p in zip(imgs, traj):
-        otsdf.integrate_cloud_frame(grid, S, img, p.R, p.t, 0.05, 0.2, clip_max=30.0, fma="blas")
+        otsdf.integrate_cloud_frame(grid, S, img, p.R, p.t, 0.05, 0.2, clip_max=30.0, fma="blas",
+                                    threads=threads)
     dt = time.perf_counter() - t0
-    return dict(value=frames / dt, unit="frames/s", cores=1, kind="port",
-                sample=f"{frames} frames of the C2 street sequence at 5 cm, oracle numpy, 1 thread")
+    return dict(value=frames / dt, unit="frames/s", cores=threads, kind="port",
+                sample=f"{frames} frames of the C2 street sequence at 5 cm, oracle numpy, "
+                       f"{threads} thread(s) (the reference's chunk pool)")
+
+
+def host_info():
+    """CPU model and numpy's BLAS, for the CPU-baseline records."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        from threadpoolctl import threadpool_info
+        info = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')} ({info[0].get('architecture')})"
+    except Exception:
+        pass
+    import numpy
+    return {"cpu_model": model, "cores": os.cpu_count(), "numpy": numpy.__version__, "blas": blas}
+
+
+def cpu_extras(tsdf_frames_1: int = 8, tsdf_frames_n: int = 16):
+    """The rest of SURVEY §8(d)'s CPU baseline, on the oracle port (bit-exact
+    with the reference, tests/test_oracle_golden.py): (i) register() latency,
+    best of 7, at threads=1 and at the reference default min(8, cores) (its
+    stride-1 shards on a thread pool); (iii) TSDF frames/s of the C2 sequence
+    at 1 and min(8, cores) threads (bounded frame counts); (iv) one
+    extract_mesh of the C3 grid after its 100-frame sequence (grid built on
+    the GPU in MATH_NP -- bit-exact with the oracle's -- and exported)."""
+    from oracle import icp as oicp
+    from oracle import image as oimg
+    from oracle import mesh as omesh
+    from oracle import sensor as osens
+    from oracle import synth as osynth
+    from oracle import tsdf as otsdf
+    from paper_2112_02779_b200 import scenes
+    threads = min(8, os.cpu_count() or 1)
+    intr = scenes.ouster64()
+    S = osens.Sensor.from_intrinsics(intr)
+    street = scenes.street_scene()
+    base, gt = scenes.pair_pool_poses(1, seed=0)[0]
+    sp = base @ gt
+    src = osynth.render(S, street, sp.R, sp.t)
+    dst = osynth.render(S, street, base.R, base.t)
+    lat = {}
+    for t in (1, threads):
+        best = 1e9
+        for _ in range(7):
+            t0 = time.perf_counter()
+            vec, valid = oimg.normals_cross(S, dst)
+            oicp.register(S, src, dst, vec, valid, fma="blas", threads=t)
+            best = min(best, time.perf_counter() - t0)
+        lat[f"threads_{t}"] = best * 1e3
+    out = {"latency_ms": dict(lat, what="normals + register() of the C1 street pair, best of 7")}
+    traj = scenes.street_trajectory(max(tsdf_frames_1, tsdf_frames_n), seed=0)
+    imgs = [osynth.render(S, street, p.R, p.t) for p in traj]
+    fps = {}
+    for t, nf in ((1, tsdf_frames_1), (threads, tsdf_frames_n)):
+        grid = {}
+        t0 = time.perf_counter()
+        for img, p in zip(imgs[:nf], traj[:nf]):
+            otsdf.integrate_cloud_frame(grid, S, img, p.R, p.t, 0.05, 0.2, clip_max=30.0, fma="blas", threads=t)
+        fps[f"threads_{t}"] = nf / (time.perf_counter() - t0)
+    out["tsdf_frames_per_s"] = dict(fps, what=f"C2 street sequence at 5 cm, first {tsdf_frames_1} / "
+                                              f"{tsdf_frames_n} frames")
+    out["marching_cubes"] = _cpu_mc_c3(omesh)
+    out["host"] = host_info()
+    return out
+
+
+def _cpu_mc_c3(omesh):
+    import paper_2112_02779_b200 as rk
+    from paper_2112_02779_b200 import pipeline, scenes
+    import torch
+    intr = scenes.hdl64()
+    traj = scenes.street_trajectory(100, seed=0)
+    frames = pipeline.render_batch(intr, scenes.street_scene(), traj)
+    grid = rk.VoxelBlockGrid(voxel_size=0.10, capacity=8192)
+    pipeline.integrate_sequence(grid, intr, frames, torch.from_numpy(pipeline.poses_to_rows(traj)).cuda(),
+                                clip_max=30.0)
+    keys, vox = grid.export_blocks()
+    og = {tuple(k): (vox[i, :, 0].reshape(16, 16, 16).copy(), vox[i, :, 1].reshape(16, 16, 16).copy())
+          for i, k in enumerate(keys.tolist())}
+    t0 = time.perf_counter()
+    V, T, _ = omesh.extract_mesh(og, 0.10)
+    ms = 1e3 * (time.perf_counter() - t0)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    m = rk.extract_mesh(grid)
+    gpu_ms = 1e3 * (time.perf_counter() - t1)
+    return {"ms": ms, "blocks": len(og), "vertices": int(len(V)), "triangles": int(len(T)),
+            "gpu_ms_public_api": gpu_ms, "gpu_same_counts": bool(m.n_vertices == len(V) and m.n_triangles == len(T)),
+            "what": "oracle extract_mesh (mesh_extract.py:85-209 restated, 1 thread) of the C3 HDL-64 "
+                    "grid at 10 cm after 100 frames; the GPU's extract_mesh of the same grid beside it"}
 
 
 # ------------------------------------------------------------------ main
@@ -584,7 +919,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
                 "config": {"workload": "C4 65,536 64x1024 street pairs (bounded CPU sample per step) "
                                        "+ C2 TSDF 5 cm", "pairs": args.pairs},
-                "cpu_baseline": icp, "tsdf": cpu_tsdf_baseline(),
+                "cpu_baseline": dict(icp, host=host_info()),
+                "tsdf": cpu_tsdf_baseline(frames=16, threads=min(8, os.cpu_count() or 1)),
                 "e2e": {"value": icp["value"], "unit": "registrations/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -599,9 +935,17 @@ def main():
         raise SystemExit("bench.py needs a CUDA device")
     r = run_ours(args, rank, world, dist)
     e2e = None if args.no_e2e else run_e2e(args, rank, world, dist, r["D"], r["tsdf"], r["cfg"])
+    extras = {}
+    if world == 1 and not args.no_extras:
+        extras["math_modes"] = run_math_modes(args, r["D"], r["cfg"])
+        extras["value_k1_per_pair"] = run_k1_per_pair(args, r["D"], r["cfg"], r["icp_kernel_ms"])
+        extras["e2e_independent"] = run_e2e_independent(args, r["D"], r["cfg"])
+        extras["kernel_rooflines"] = kernel_rooflines(args, r["D"], r, r["tsdf"])
+        extras["c5_tsdf"] = run_c5_tsdf()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_icp_baseline(args.cpu_seconds)
+        cpu.update(cpu_extras())
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -646,6 +990,12 @@ def main():
         "clocks": r["clocks"], "gpu_launches": r["launches"],
         "e2e": e2e, "cpu_baseline": cpu,
     }
+    line.update(extras)
+    line["math"] = {"headline": "np (numpy-exact projection: the reference's decisions and per-point "
+                                "terms bit for bit)", "others": "math_modes"}
+    line["pool_reuse"] = ("value/e2e reuse a pool of %d device-rendered pairs: K1 once per pool image and "
+                          "16.4 KB of H2D per registration; value_k1_per_pair and e2e_independent charge "
+                          "K1 and 512 KB of H2D to every pair" % args.pool)
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

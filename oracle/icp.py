@@ -175,27 +175,74 @@ class DegenerateGeometryError(Exception):
     pass
 
 
+def _shard_bounds(n, shards):
+    """registration.py:292-296: one shard below 40,000 points or 1 thread."""
+    if shards <= 1 or n < 40_000:
+        return [(0, n)]
+    edges = np.linspace(0, n, shards + 1).astype(int)
+    return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+def _normal_equations_sharded(sensor, src, dst_rng, dst_nrm, dst_valid, R, t, gate, stride, kern,
+                              shards, pool, math, fma):
+    """_accumulate_normal_equations (registration.py:299-326): per-shard
+    association + float32 partial systems (on the thread pool), merged in
+    shard order in float64."""
+    def run(ab):
+        a, b = ab
+        sel, tgt, nrm, _ = correspondences_f32(sensor, src[a:b], dst_rng, dst_nrm, dst_valid,
+                                               R, t, gate, stride, math=math, fma=fma)
+        return normal_equations_f32(src[a:b][sel], tgt, nrm, R, t, kern, fma=fma)
+    parts = list(pool.map(run, shards)) if pool is not None and len(shards) > 1 else [run(s) for s in shards]
+    n = sum(p[0] for p in parts)
+    Hm, b, cost, sumsq = np.zeros((6, 6)), np.zeros(6), 0.0, 0.0
+    for ni, Hi, bi, ci, si in parts:
+        if ni:
+            Hm += Hi
+            b += bi
+            cost += ci
+            sumsq += si
+    return n, Hm, b, cost, sumsq
+
+
 def register(sensor, src_rng, dst_rng, dst_nrm, dst_valid, R0=None, t0=None, *,
              kernel_scale=0.5, max_dist=0.5, schedule=DEFAULT_SCHEDULE, rot_eps=1e-4,
              trans_eps=1e-4, clip_min=0.0, clip_max=np.inf, min_corr=6,
-             scale_with_stride=True, math="numpy", fma="exact"):
-    """Coarse-to-fine ICP with a single shard (registration.py:237-289, threads=1).
+             scale_with_stride=True, math="numpy", fma="exact", threads=1):
+    """Coarse-to-fine ICP (registration.py:237-289).  threads > 1 shards the
+    levels of >= 40,000 points over a thread pool exactly as the reference
+    does (its RANGEKIT_THREADS / RegistrationConfig.threads); threads=1 is
+    the single-shard schedule the goldens were made with.
 
     Returns dict(R, t, converged, stats=[(stride, it, n, cost, rmse)], degenerate).
     """
+    from concurrent.futures import ThreadPoolExecutor
     R = EYE3.copy() if R0 is None else np.asarray(R0, dtype=float).copy()
     t = np.zeros(3) if t0 is None else np.asarray(t0, dtype=float).copy()
     stats = []
+    pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
+    try:
+        return _register_levels(sensor, src_rng, dst_rng, dst_nrm, dst_valid, R, t, stats, pool, threads,
+                                kernel_scale, max_dist, schedule, rot_eps, trans_eps, clip_min, clip_max,
+                                min_corr, scale_with_stride, math, fma)
+    finally:
+        if pool is not None:
+            pool.shutdown(wait=False)
+
+
+def _register_levels(sensor, src_rng, dst_rng, dst_nrm, dst_valid, R, t, stats, pool, threads,
+                     kernel_scale, max_dist, schedule, rot_eps, trans_eps, clip_min, clip_max,
+                     min_corr, scale_with_stride, math, fma):
     for stride, iters in schedule:
         level = float(stride) if scale_with_stride else 1.0
         gate = max_dist * level
         kern = kernel_scale * level
         src = points_at_stride(sensor, src_rng, stride, clip_min, clip_max)
+        shards = _shard_bounds(src.shape[0], threads if pool else 1)
         for it in range(iters):
-            sel, tgt, nrm, _ = correspondences_f32(sensor, src, dst_rng, dst_nrm, dst_valid,
-                                                   R, t, gate, stride, math=math, fma=fma)
-            n, Hm, b, cost, sumsq = normal_equations_f32(src[sel], tgt, nrm, R, t, kern,
-                                                         fma=fma)
+            n, Hm, b, cost, sumsq = _normal_equations_sharded(sensor, src, dst_rng, dst_nrm, dst_valid,
+                                                              R, t, gate, stride, kern, shards, pool,
+                                                              math, fma)
             if n < min_corr:
                 return dict(R=R, t=t, converged=False, stats=stats, degenerate=False)
             if np.linalg.cond(Hm) > 1e12:

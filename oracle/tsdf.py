@@ -70,7 +70,7 @@ def _chunk_centres(keys, R_inv, t_inv, voxel, fma="exact", lone=None):
 
 def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
               free_space=True, clip_min=0.0, clip_max=np.inf, math="numpy", fma="exact",
-              touched=None):
+              touched=None, threads=1):
     """Projective running-average update of the given blocks (lines 116-186).
 
     (R, t) maps the frame into the world; its inverse is formed with numpy as
@@ -80,6 +80,8 @@ def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
     gets inside this larger touched set (the reference chunks the sorted set
     in 146-block tasks; only a lone last block is computed differently), so a
     sample of blocks can be checked without integrating the whole frame.
+    ``threads`` > 1 runs the chunks on a thread pool as the reference does
+    (sdf_volume.py:144-151); the result does not depend on it.
     """
     R = np.asarray(R, dtype=float)
     t = np.asarray(t, dtype=float)
@@ -89,7 +91,6 @@ def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
     img = np.asarray(rng, dtype=F32)
     W = sensor.W
     tau = F32(trunc)
-    updated = 0
     lone_key = None
     if touched is None:
         chunks = [order[i0:i0 + CHUNK_BLOCKS] for i0 in range(0, len(order), CHUNK_BLOCKS)]
@@ -101,7 +102,8 @@ def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
         chunks = [rest[i0:i0 + CHUNK_BLOCKS] for i0 in range(0, len(rest), CHUNK_BLOCKS)]
         if lone_key is not None and lone_key in set(order):
             chunks.append([lone_key])
-    for part in chunks:
+
+    def one(part):
         lone = None if touched is None else (part == [lone_key])
         x = _chunk_centres(part, R_inv, t_inv, voxel, fma=fma, lone=lone)
         u, v, r, status = sensor.project_f32(x, math=math)
@@ -123,13 +125,20 @@ def integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight=100.0,
         for j, k in enumerate(part):
             grid[k] = (ts_new[j * VOXELS:(j + 1) * VOXELS].reshape((EDGE,) * 3),
                        ws_new[j * VOXELS:(j + 1) * VOXELS].reshape((EDGE,) * 3))
-        updated += int(np.count_nonzero(ok))
+        return int(np.count_nonzero(ok))
+
+    if threads > 1 and len(chunks) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            updated = sum(ex.map(one, chunks))
+    else:
+        updated = sum(one(part) for part in chunks)
     return updated
 
 
 def integrate_cloud_frame(grid, sensor, rng, R, t, voxel, trunc, max_weight=100.0,
                           free_space=True, radius=None, clip_min=0.0, clip_max=np.inf,
-                          math="numpy", fma="exact"):
+                          math="numpy", fma="exact", threads=1):
     """activate + integrate for one posed frame (lines 198-210)."""
     from .image import to_point_cloud
 
@@ -138,7 +147,7 @@ def integrate_cloud_frame(grid, sensor, rng, R, t, voxel, trunc, max_weight=100.
     world = rows_times_mat_t(pts, R, t, mode=fma)
     keys = activate(grid, world, radius, EDGE * voxel)
     n = integrate(grid, sensor, rng, R, t, keys, voxel, trunc, max_weight, free_space,
-                  clip_min, clip_max, math=math, fma=fma)
+                  clip_min, clip_max, math=math, fma=fma, threads=threads)
     return keys, n
 
 
