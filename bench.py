@@ -319,11 +319,13 @@ def run_ours(args, rank, world, dist):
         dist.barrier()
         torch.cuda.synchronize()
         t_mc = time.perf_counter()
-        m = tsdf.sharded.extract_mesh()
+        m = tsdf.sharded.extract_mesh(root=0)
         torch.cuda.synchronize()
-        mesh = {"ms": 1e3 * (time.perf_counter() - t_mc), "vertices": int(m.vertices.shape[0]),
-                "triangles": int(m.triangles.shape[0]), "blocks_this_rank": int(n_blocks),
-                "distributed": True}
+        mesh = {"ms": 1e3 * (time.perf_counter() - t_mc), "blocks_this_rank": int(n_blocks),
+                "distributed": True, "what": "halo all-to-all, per-rank MC, gather to rank 0, "
+                                             "device merge by exact position"}
+        if m is not None:
+            mesh.update(vertices=int(m.vertices.shape[0]), triangles=int(m.triangles.shape[0]))
     # C2 end to end (outside the timed region, wall clock incl. its one host
     # sync): frame-to-frame odometry of the sequence (one register_batch of
     # F-1 pairs + the host pose prefix product, cli.py:248-263) and the

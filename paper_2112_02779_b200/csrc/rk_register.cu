@@ -615,8 +615,18 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
               d_next = make_double3(__ldg(dp), __ldg(dp + 1), __ldg(dp + 2));
             }
             if (!range_ok(r, cmin, cmax)) continue;
-            associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
-                                               lvl_w, inv_s, gate2, inv_k, k32, acc, cost, sumsq, cnt);
+            if (RK_ICP_LVL_SMEM) {
+              // the level constants from shared memory (under the register
+              // cap the compiler would otherwise re-derive them per point)
+              const float4 L0 = sh_lvl[g][0], L1 = sh_lvl[g][1];
+              associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, sh_surf[g], rec,
+                                                 __float_as_int(L0.w), __float_as_int(L1.x),
+                                                 __float_as_int(L1.y), L0.z, L0.x, L0.y, L1.z, acc, cost,
+                                                 sumsq, cnt);
+            } else {
+              associate_point<MATH, SMEM, STATS>(s, tb, pose, r, dcur, ocur, surf, rec, stride, lvl_off,
+                                                 lvl_w, inv_s, gate2, inv_k, k32, acc, cost, sumsq, cnt);
+            }
           }
         }
       } else if (col_mode) {

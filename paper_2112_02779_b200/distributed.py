@@ -9,8 +9,9 @@ shard:
   count / largest key are reduced so every rank reproduces the reference's
   sorted-chunk arithmetic.  Meshing: each rank receives the halo blocks it
   needs (26-neighbours owned elsewhere) in one all-to-all, runs marching
-  cubes on its own blocks, and the partial meshes are gathered and merged by
-  exact vertex position (the reference's own dedup rule).
+  cubes on its own blocks, and the partial meshes are gathered to one rank
+  and merged there on the device by exact vertex position (the reference's
+  own dedup rule).
 
 The communication helpers take plain tensors so they run under the ``gloo``
 backend on CPU as well (tests/test_distributed.py); ``ShardedGrid`` adds the
@@ -67,6 +68,77 @@ def all_gather_varsize(t, dist=None):
     bufs = [torch.empty_like(pad) for _ in range(world)]
     d.all_gather(bufs, pad)
     return torch.cat([b[:c] for b, c in zip(bufs, counts)])
+
+
+def gather_varsize_to(t, dst: int = 0, dist=None):
+    """Gather tensors whose first dimension differs per rank onto rank
+    ``dst`` only (counts all-gathered first, then one padded gather); returns
+    the rank-order concatenation on ``dst`` and None elsewhere."""
+    import torch
+    import torch.distributed as tdist
+    d = dist or tdist
+    world, rank = d.get_world_size(), d.get_rank()
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    d.all_gather(counts, n)
+    counts = [int(c.item()) for c in counts]
+    width = max(counts) if counts else 0
+    pad = torch.zeros((width,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[:t.shape[0]] = t
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    d.gather(pad, bufs, dst=dst)
+    if rank != dst:
+        return None
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)])
+
+
+class CpuStagedDist:
+    """torch.distributed's collectives for CUDA tensors over a CPU-only
+    backend (gloo): every call stages through host memory.  Lets several
+    ranks share one GPU in tests (the driver's boxes have one B200); the
+    production path passes torch.distributed itself (NCCL)."""
+
+    def __init__(self, dist=None):
+        import torch.distributed as tdist
+        self.d = dist or tdist
+        self.ReduceOp = self.d.ReduceOp
+
+    def get_world_size(self):
+        return self.d.get_world_size()
+
+    def get_rank(self):
+        return self.d.get_rank()
+
+    def barrier(self):
+        self.d.barrier()
+
+    def broadcast(self, t, src):
+        h = t.cpu()
+        self.d.broadcast(h, src)
+        t.copy_(h)
+
+    def all_reduce(self, t, op=None):
+        h = t.cpu()
+        self.d.all_reduce(h, op=op or self.d.ReduceOp.SUM)
+        t.copy_(h)
+
+    def all_gather(self, out, t):
+        hs = [o.cpu() for o in out]
+        self.d.all_gather(hs, t.cpu())
+        for o, h in zip(out, hs):
+            o.copy_(h)
+
+    def gather(self, t, gather_list=None, dst=0):
+        hs = [o.cpu() for o in gather_list] if gather_list is not None else None
+        self.d.gather(t.cpu(), hs, dst=dst)
+        if gather_list is not None:
+            for o, h in zip(gather_list, hs):
+                o.copy_(h)
+
+    def all_to_all_single(self, out, inp, out_split=None, in_split=None):
+        h = out.cpu()
+        self.d.all_to_all_single(h, inp.cpu(), out_split, in_split)
+        out.copy_(h)
 
 
 def broadcast_frames(frames, poses, src: int = 0, dist=None):
@@ -221,46 +293,51 @@ class ShardedGrid:
         g.blocks._bump()
         return upd.clone() if own_upd else upd
 
-    def extract_mesh(self, min_weight: float = 1.0):
-        """Distributed marching cubes: one all-to-all of halo blocks, MC on the
-        owned blocks, one gather of the partial meshes, exact-position merge.
-        Returns a host TriangleMesh on every rank."""
+    def extract_mesh(self, min_weight: float = 1.0, root: int = 0):
+        """Distributed marching cubes: the block keys are all-gathered (12 B
+        per block) and every rank derives the halo plan on the device; one
+        all-to-all moves the halo blocks; each rank meshes its own blocks; the
+        partial meshes are gathered to ``root`` only and merged there on the
+        device by exact vertex position (the reference's dedup rule,
+        mesh_extract.py:146-151, which also joins the edges both neighbouring
+        ranks produce on a shard boundary).  Returns a host TriangleMesh on
+        ``root`` and None on the other ranks."""
         import torch
 
         from .mesh_extract import TriangleMesh
         d, world, rank = self.dist, self.world, self.rank
         keys, vox = self.grid.export_blocks(device=True)
         if world == 1:
-            V, T, N = merge_meshes([mesh_from_shard(self.grid, 0, 1, min_weight=min_weight)])
-            return TriangleMesh(V, T, N)
-        all_keys = all_gather_varsize(keys, d)
+            V, T, N = merge_meshes_device([mesh_from_shard(self.grid, 0, 1, min_weight=min_weight)])
+            return TriangleMesh(nat.to_host(V), nat.to_host(T), nat.to_host(N))
         n = torch.tensor([keys.shape[0]], dtype=torch.int64, device=keys.device)
         counts = [torch.zeros_like(n) for _ in range(world)]
         d.all_gather(counts, n)
         counts = [int(c.item()) for c in counts]
-        host = nat.to_host(all_keys)
+        all_keys = all_gather_varsize(keys, d)
         bounds = np.cumsum([0] + counts)
-        plan = halo_plan([host[bounds[q]:bounds[q + 1]] for q in range(world)])
-        send_idx = np.concatenate([plan[rank][s_] for s_ in range(world)]).astype(np.int64)
-        in_split = [int(plan[rank][s_].size) for s_ in range(world)]
-        out_split = [int(plan[q][rank].size) for q in range(world)]
-        sel = torch.from_numpy(send_idx).to(keys.device)
+        by_rank = [all_keys[bounds[q]:bounds[q + 1]] for q in range(world)]
+        send = halo_send(by_rank, rank)                      # my blocks each rank needs
+        recv_n = [int(halo_send(by_rank, q, only=rank)[rank].numel()) for q in range(world)]
+        in_split = [int(send[q].numel()) for q in range(world)]
+        sel = torch.cat(send) if send else torch.zeros(0, dtype=torch.int64, device=keys.device)
         k_send = keys[sel].contiguous()
         v_send = vox[sel].reshape(-1, 8192).contiguous()
-        k_recv = torch.empty((sum(out_split), 3), dtype=keys.dtype, device=keys.device)
-        v_recv = torch.empty((sum(out_split), 8192), dtype=vox.dtype, device=vox.device)
-        d.all_to_all_single(k_recv, k_send, out_split, in_split)
-        d.all_to_all_single(v_recv, v_send, out_split, in_split)
+        k_recv = torch.empty((sum(recv_n), 3), dtype=keys.dtype, device=keys.device)
+        v_recv = torch.empty((sum(recv_n), 8192), dtype=vox.dtype, device=vox.device)
+        d.all_to_all_single(k_recv, k_send, recv_n, in_split)
+        d.all_to_all_single(v_recv, v_send, recv_n, in_split)
         V, T, N = mesh_from_shard(self.grid, rank, world, k_recv, v_recv, min_weight)
-        nv = torch.tensor([V.shape[0]], dtype=torch.int64, device=V.device)
-        nvs = [torch.zeros_like(nv) for _ in range(world)]
-        d.all_gather(nvs, nv)
+        nvs = [torch.zeros(1, dtype=torch.int64, device=V.device) for _ in range(world)]
+        d.all_gather(nvs, torch.tensor([V.shape[0]], dtype=torch.int64, device=V.device))
         base = sum(int(c.item()) for c in nvs[:rank])
-        Vg = all_gather_varsize(V, d)
-        Ng = all_gather_varsize(N, d)
-        Tg = all_gather_varsize(T.to(torch.int64) + base, d)
-        Vm, Tm, Nm = merge_meshes([(Vg, Tg, Ng)])
-        return TriangleMesh(Vm, Tm, Nm)
+        Vg = gather_varsize_to(V, root, d)
+        Ng = gather_varsize_to(N, root, d)
+        Tg = gather_varsize_to(T.to(torch.int64) + base, root, d)
+        if rank != root:
+            return None
+        Vm, Tm, Nm = merge_meshes_device([(Vg, Tg, Ng)])
+        return TriangleMesh(nat.to_host(Vm), nat.to_host(Tm), nat.to_host(Nm))
 
     def gather_blocks(self):
         """All ranks' (keys (n,3) int32, voxels (n,4096,2) float32), device, rank order."""
@@ -299,22 +376,42 @@ def _codes(keys) -> np.ndarray:
     return (k[:, 0] << 36) | (k[:, 1] << 18) | k[:, 2]   # sdf_volume.py:64-71 packing
 
 
-def halo_plan(keys_by_rank):
-    """send[r][s]: indices into rank r's block list of the blocks rank s needs
-    as halo (26-neighbours of s's blocks that r owns; marching cubes reads a
-    19^3 window, mesh_extract.py:58-82).  Identical on every rank."""
+def _codes_t(keys):
+    """sdf_volume.py:64-71 packing of (n, 3) integer keys, torch (any device)."""
+    import torch
+    k = keys.to(torch.int64).reshape(-1, 3) + (1 << 17)
+    return (k[:, 0] << 36) | (k[:, 1] << 18) | k[:, 2]
+
+
+def halo_send(keys_by_rank, r: int, only: int | None = None):
+    """send[s]: indices into rank r's block list (a torch tensor on any
+    device) of the blocks rank s needs as halo -- the 26-neighbours of s's
+    blocks that r owns (marching cubes reads a 19^3 window,
+    mesh_extract.py:58-82).  ``only`` restricts the work to one s."""
+    import torch
     world = len(keys_by_rank)
-    codes = [_codes(k) for k in keys_by_rank]
-    send = [[np.zeros(0, np.int64) for _ in range(world)] for _ in range(world)]
+    kr = keys_by_rank[r]
+    dev = kr.device
+    neigh = torch.from_numpy(_NEIGH).to(dev)
+    codes_r = _codes_t(kr)
+    out = [torch.zeros(0, dtype=torch.int64, device=dev) for _ in range(world)]
     for s_ in range(world):
-        k = np.asarray(keys_by_rank[s_], dtype=np.int64).reshape(-1, 3)
-        if k.shape[0] == 0:
+        if s_ == r or (only is not None and s_ != only):
             continue
-        need = np.unique(_codes((k[:, None, :] + _NEIGH[None]).reshape(-1, 3)))
-        for r in range(world):
-            if r != s_ and codes[r].size:
-                send[r][s_] = np.flatnonzero(np.isin(codes[r], need))
-    return send
+        ks = keys_by_rank[s_].to(torch.int64).reshape(-1, 3)
+        if ks.shape[0] == 0 or codes_r.numel() == 0:
+            continue
+        need = _codes_t((ks[:, None, :] + neigh[None]).reshape(-1, 3))
+        out[s_] = torch.nonzero(torch.isin(codes_r, need)).reshape(-1)
+    return out
+
+
+def halo_plan(keys_by_rank):
+    """send[r][s] for every pair of ranks as host index arrays (the same
+    device computation, ``halo_send``, run per rank)."""
+    import torch
+    kt = [torch.as_tensor(np.asarray(k, dtype=np.int64).reshape(-1, 3)) for k in keys_by_rank]
+    return [[x.cpu().numpy() for x in halo_send(kt, r)] for r in range(len(kt))]
 
 
 def mesh_from_shard(grid, rank: int, world: int, halo_keys=None, halo_vox=None,
@@ -335,22 +432,34 @@ def mesh_from_shard(grid, rank: int, world: int, halo_keys=None, halo_vox=None,
     return extract_mesh_device(tmp, min_weight)
 
 
-def merge_meshes(parts):
-    """Concatenate per-rank (V, T, N) meshes and merge vertices that sit at
-    the same exact position (edges on shard boundaries are produced by both
-    neighbouring ranks).  Returns host (V, T, N)."""
-    Vs = [np.asarray(nat.to_host(v) if nat.is_tensor(v) else v, dtype=np.float64).reshape(-1, 3)
-          for v, _, _ in parts]
-    Ts, Ns, base = [], [], 0
-    for (v, t, n), V in zip(parts, Vs):
-        T = np.asarray(nat.to_host(t) if nat.is_tensor(t) else t, dtype=np.int64).reshape(-1, 3)
-        Ts.append(T + base)
-        Ns.append(np.asarray(nat.to_host(n) if nat.is_tensor(n) else n, dtype=np.float64).reshape(-1, 3))
-        base += V.shape[0]
-    V = np.concatenate(Vs) if Vs else np.zeros((0, 3))
-    N = np.concatenate(Ns) if Ns else np.zeros((0, 3))
-    T = np.concatenate(Ts) if Ts else np.zeros((0, 3), np.int64)
+def merge_meshes_device(parts):
+    """Concatenate per-rank (V, T, N) meshes (tensors on one device) and merge
+    vertices at the same exact float64 position, keeping each position's
+    first normal -- np.unique(V, axis=0) semantics (lexicographically sorted
+    unique positions), on the device.  Returns (V, T int32, N) tensors."""
+    import torch
+    Vs, Ts, Ns, base = [], [], [], 0
+    for v, t, n in parts:
+        v = torch.as_tensor(v, dtype=torch.float64).reshape(-1, 3)
+        Vs.append(v)
+        Ts.append(torch.as_tensor(t).to(device=v.device, dtype=torch.int64).reshape(-1, 3) + base)
+        Ns.append(torch.as_tensor(n, dtype=torch.float64).to(v.device).reshape(-1, 3))
+        base += v.shape[0]
+    V, T, N = torch.cat(Vs), torch.cat(Ts), torch.cat(Ns)
     if V.shape[0] == 0:
-        return V, T.astype(np.int32), N
-    uniq, first, inv = np.unique(V, axis=0, return_index=True, return_inverse=True)
-    return uniq, inv.reshape(-1)[T].astype(np.int32), N[first]
+        return V, T.to(torch.int32), N
+    # -0.0 and 0.0 are one position for np.unique (they compare equal)
+    V = V + 0.0
+    uniq, inv = torch.unique(V, dim=0, return_inverse=True)
+    pos = torch.arange(V.shape[0], device=V.device)
+    first = torch.full((uniq.shape[0],), V.shape[0], dtype=torch.int64, device=V.device)
+    first = first.scatter_reduce(0, inv, pos, reduce="amin")
+    return uniq, inv[T].to(torch.int32), N[first]
+
+
+def merge_meshes(parts):
+    """Host wrapper of merge_meshes_device: returns numpy (V, T, N)."""
+    import torch
+    parts = [tuple(x if nat.is_tensor(x) else torch.as_tensor(np.asarray(x)) for x in p) for p in parts]
+    V, T, N = merge_meshes_device(parts)
+    return V.cpu().numpy(), T.cpu().numpy(), N.cpu().numpy()
