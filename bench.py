@@ -903,8 +903,21 @@ def dist_init(args):
     import torch
     import torch.distributed as dist
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("RK_BENCH_GLOO"):
+        # functional check of the N > 1 path on a one-GPU box: every rank on
+        # cuda:0, collectives staged through host memory over gloo (timings
+        # are not scaling numbers)
+        from paper_2112_02779_b200.distributed import CpuStagedDist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        staged = CpuStagedDist(dist)
+        staged.destroy_process_group = dist.destroy_process_group
+        return staged, dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl")
+    if dist.get_rank() == 0:
+        print(f"[bench] NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, world {dist.get_world_size()}, "
+              f"backend {dist.get_backend()}", file=sys.stderr)
     return dist, dist.get_rank(), dist.get_world_size()
 
 
