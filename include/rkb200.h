@@ -85,7 +85,8 @@ int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, int math,
 /* diagnostic: RK_MATH_NP's arithmetic elementwise on device arrays --
  * fn 0: out = np.arctan2(a, b) (lidar_model.py:288), fn 1: out = np.arcsin(a)
  * (lidar_model.py:45; |a| <= 1), fn 2: the kernels' range-check-free
- * division a / b, fn 3: IEEE a / b; float32 (parity tests) */
+ * division a / b, fn 3: IEEE a / b, fn 4: the kernels' square root for
+ * operands in [2^-101, 2^128), fn 5: IEEE sqrt(a); float32 (parity tests) */
 int rk_svml_eval(const rk_sensor* s, int fn, const float* a, const float* b, int64_t n,
                  float* out, void* stream);
 /* project_many(single=False) float64 fixed-point path, lidar_model.py:287-344.

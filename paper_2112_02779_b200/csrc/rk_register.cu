@@ -292,7 +292,7 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   if (EXACT) {
     e = div_rn_fast(res, k32);
     s1 = __fadd_rn(1.0f, __fmul_rn(e, e));
-    w = div_rn_fast(1.0f, __fsqrt_rn(s1));
+    w = div_rn_fast(1.0f, (RK_SQRT_FAST && s1 < 3.0e38f) ? sqrt_rn_normal(s1) : __fsqrt_rn(s1));  // s1 >= 1
   } else {
     e = res * inv_k;
     s1 = __fmaf_rn(e, e, 1.0f);

@@ -147,14 +147,19 @@ __global__ void k_svml_eval(SensorDev s, int fn, const float* __restrict__ a, co
     out[i] = fn == 0   ? svml_atan2f(a[i], b[i])
              : fn == 1 ? svml_asinf(a[i], s.rsqrt14)
              : fn == 2 ? div_rn_fast(a[i], b[i])
-                       : __fdiv_rn(a[i], b[i]);
+             : fn == 3 ? __fdiv_rn(a[i], b[i])
+             : fn == 4 ? sqrt_rn_normal(a[i])
+                       : __fsqrt_rn(a[i]);
 }
 
 extern "C" int rk_svml_eval(const rk_sensor* s, int fn, const float* a, const float* b, int64_t n,
                             float* out, void* stream) {
   if (n <= 0) return RK_OK;
-  if (fn < 0 || fn > 3) { rk_set_error("fn must be 0 (arctan2), 1 (arcsin), 2 / 3 (division)"); return RK_EGENERIC; }
-  if (fn != 1 && !b) { rk_set_error("arctan2 and division need b"); return RK_EGENERIC; }
+  if (fn < 0 || fn > 5) {
+    rk_set_error("fn must be 0 (arctan2), 1 (arcsin), 2 / 3 (division), 4 / 5 (square root)");
+    return RK_EGENERIC;
+  }
+  if ((fn == 0 || fn == 2 || fn == 3) && !b) { rk_set_error("arctan2 and division need b"); return RK_EGENERIC; }
   unsigned g = min(blocks_for(n, 256), 148u * 16u);
   k_svml_eval<<<g, 256, 0, S(stream)>>>(s->dev, fn, a, b, n, out);
   RK_LAUNCHED("k_svml_eval");
