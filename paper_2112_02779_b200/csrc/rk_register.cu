@@ -855,12 +855,28 @@ cudaLaunchConfig_t cluster_config(int batch, cudaStream_t st, cudaLaunchAttribut
 
 // how many CL-CTA clusters are co-resident on this device (GPC packing:
 // 148 SMs do not hold 18 clusters of 8 full-SM CTAs); cached per device
+// clusters above the portable size 8 need the per-kernel opt-in
+template <int MATH, int CL, int NT = kWide>
+void allow_cluster_size() {
+  if (CL <= 8) return;
+  constexpr int WPP = NT / 32;
+  cudaFuncSetAttribute(k_register<MATH, WPP, 1, true, true, NT, CL>,
+                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_register<MATH, WPP, 1, false, true, NT, CL>,
+                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_register<MATH, WPP, 1, true, false, NT, CL>,
+                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_register<MATH, WPP, 1, false, false, NT, CL>,
+                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
 template <int CL>
 int max_active_clusters() {
   static int cache[64] = {0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
   if (!cache[dev]) {
+    allow_cluster_size<MATH_FAST, CL>();
     cudaLaunchAttribute at[1];
     cudaLaunchConfig_t lc = cluster_config<CL>(1, nullptr, at);
     int n = 0;
@@ -880,6 +896,15 @@ template <int MATH, int CL, int NT = kWide>
 int launch_cluster(const IcpArgs& a, cudaStream_t st) {
   constexpr int WPP = NT / 32;
   const bool smem = a.s.H <= kMaxRowsSmem && a.s.K <= kMaxInvSmem;
+  if (CL > 8) {
+    static bool allowed[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !allowed[dev]) {
+      allow_cluster_size<MATH, CL, NT>();
+      allowed[dev] = true;
+    }
+  }
   cudaLaunchAttribute at[1];
   cudaLaunchConfig_t lc = cluster_config<CL, NT>(a.batch, st, at);
   cudaError_t e;
@@ -938,6 +963,7 @@ int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) 
                                  : batch <= max_active_clusters<4>() ? 4
                                  : batch <= max_active_clusters<2>() ? 2
                                                                      : 1);
+      if (cl == 16) return launch_cluster<MATH, 16>(a, st);
       if (cl == 8) return launch_cluster<MATH, 8>(a, st);
       if (cl == 4) return launch_cluster<MATH, 4>(a, st);
       if (cl == 2) return launch_cluster<MATH, 2>(a, st);
