@@ -17,6 +17,6 @@ for spec in ${SPECS:-base:np}; do
   if [ "$v" = "base" ]; then lib=$PWD/paper_2112_02779_b200/lib/librkb200.so; else lib=$PWD/paper_2112_02779_b200/lib/librkb200_$v.so; fi
   RK_LIB=$lib timeout 300 python bench.py $SMALL --math $m > $OUT/ab_${v}_$m.json 2> $OUT/ab_${v}_$m.err
   echo -n "$v/$m rc=$? "
-  python -c "import json; d=json.load(open('$OUT/ab_${v}_$m.json')); print('reg/s', round(d['value']), 'K3 ms', round(d['phase_ms']['register'],2), 'frac', round(d['roofline']['frac'],4), 'tsdf fps', round(d['tsdf']['value']), 'tsdf ms', round(d['phase_ms']['tsdf_sequence'],3), 'gt', d['gt_recovered_frac'])" 2>&1 | tail -1
+  python -c "import json; d=json.load(open('$OUT/ab_${v}_$m.json')); print('reg/s', round(d['value']), 'K1 ms', round(d['phase_ms']['normals'],3), 'K3 ms', round(d['phase_ms']['register'],2), 'frac', round(d['roofline']['frac'],4), 'tsdf fps', round(d['tsdf']['value']), 'tsdf ms', round(d['phase_ms']['tsdf_sequence'],3), 'gt', d['gt_recovered_frac'])" 2>&1 | tail -1
 done
 done
