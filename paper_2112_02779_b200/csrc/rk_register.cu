@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
   __shared__ double sh_pose[GROUPS][12];
   __shared__ double sh_red[NW][kNumAcc];
   __shared__ double sh_tot[GROUPS][kNumAcc];
+  __shared__ double sh_part[CL][kNumAcc + 1];  // CL > 1: the cluster's partials, in the lead CTA
   __shared__ int sh_cnt[NW];
   __shared__ int sh_ctrl[GROUPS];
   __shared__ float sh_pose32[GROUPS][12];
@@ -720,17 +721,26 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
       }
       group_sync<WPP, NT>(g);
       if (CL > 1) {
-        // the cluster's partial systems -> the lead CTA, in rank order
+        // the cluster's partial systems -> the lead CTA: every other CTA
+        // stores its partial into the lead's shared memory (posted DSMEM
+        // stores, no round trips), the cluster barrier publishes them, and
+        // the lead sums them in rank order (deterministic)
         cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        if (!lead && gtid <= kNumAcc) {
+          if (gtid < kNumAcc)
+            cl.map_shared_rank(&sh_part[0][0], 0)[crank * (kNumAcc + 1) + gtid] = tot[gtid];
+          else
+            cl.map_shared_rank(&sh_part[0][0], 0)[crank * (kNumAcc + 1) + kNumAcc] = (double)sh_cnt[0];
+        }
         cl.sync();
         if (lead && gtid <= kNumAcc) {
           if (gtid < kNumAcc) {
             double t = tot[gtid];
-            for (int r = 1; r < CL; ++r) t += cl.map_shared_rank(tot, r)[gtid];
+            for (int r = 1; r < CL; ++r) t += sh_part[r][gtid];
             tot[gtid] = t;
           } else {
             int c = sh_cnt[0];
-            for (int r = 1; r < CL; ++r) c += cl.map_shared_rank(&sh_cnt[0], r)[0];
+            for (int r = 1; r < CL; ++r) c += (int)sh_part[r][kNumAcc];
             sh_cnt[0] = c;
           }
         }
