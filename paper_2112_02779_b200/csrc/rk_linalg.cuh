@@ -138,7 +138,8 @@ __device__ inline void se3_left_update(const double* xi, double* pose) {
       V[i] = I + 0.5 * K[i];
     }
   } else {
-    const double s = sin(th), c = cos(th);
+    double s, c;
+    sincos(th, &s, &c);  // one shared argument reduction (same values as sin / cos)
     hat3(w0 / th, w1 / th, w2 / th, K);
     mat3_mul(K, K, K2);
     double Kw[9], Kw2[9];
