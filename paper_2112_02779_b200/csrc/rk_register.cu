@@ -43,6 +43,9 @@ using namespace rk;
 #ifndef RK_ICP_F64_AHEAD
 #define RK_ICP_F64_AHEAD 1
 #endif
+#ifndef RK_ICP_TRANSPOSE  // recursive-halving warp reduction of the partials (1) or 29 butterfly sums (0)
+#define RK_ICP_TRANSPOSE 1
+#endif
 #ifndef RK_ICP_ELEV_ONLY
 #define RK_ICP_ELEV_ONLY 1
 #endif
@@ -233,6 +236,42 @@ __device__ __forceinline__ int warp_solve_step(const double* tot, int n_corr, do
     ctrl = (nr < rot_eps && nt < trans_eps) ? 1 : 0;
   }
   return __shfl_sync(0xffffffffu, ctrl, 0);
+}
+
+// The warp's 29 per-lane partials (27 normal-equation terms, cost, sum of
+// squares) reduced by recursive halving: at each step a lane keeps one half
+// of its values and adds the partner's copy of the same half, so after five
+// steps lane L holds the warp total of value L.  46 shuffles instead of the
+// 290 of 29 separate butterfly sums (the shuffle pipe moves one warp per
+// clock per SM).  The first step adds the float32 partials in float32, the
+// rest run in float64; the tree is fixed, so the result is deterministic.
+// Returns lane L's total (L < 29; lanes 29-31 hold zero padding).
+template <bool STATS>
+__device__ __forceinline__ double warp_transpose_sum(const float* acc, float cost, float sumsq) {
+  const int lane = threadIdx.x & 31;
+  auto val = [&](int i) -> float {
+    return i < 27 ? acc[i] : (i == 27 ? (STATS ? cost : 0.0f) : (i == 28 ? (STATS ? sumsq : 0.0f) : 0.0f));
+  };
+  double v[16];
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float lo = val(i), hi = val(i + 16);
+      const float r = __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
+      v[i] = (double)__fadd_rn(up ? hi : lo, r);
+    }
+  }
+#pragma unroll
+  for (int k = 8; k >= 1; k >>= 1) {
+    const bool up = lane & k;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const double r = __shfl_xor_sync(0xffffffffu, up ? v[i] : v[i + k], k);
+      v[i] = (up ? v[i + k] : v[i]) + r;
+    }
+  }
+  return v[0];
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -684,20 +723,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
       }
       // ---- deterministic group reduction in float64
       double* tot = sh_tot[g];
-      if (WPP == 1) {
-#pragma unroll
-        for (int i = 0; i < 27; ++i) {
-          const double v = warp_sum((double)acc[i]);
-          if (lane == 0) tot[i] = v;
-        }
-        const double c = warp_sum((double)cost), q2 = warp_sum((double)sumsq);
-        const int nc = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) {
-          tot[27] = c;
-          tot[28] = q2;
-          sh_cnt[warp] = nc;
-        }
-      } else {
+      if (!RK_ICP_TRANSPOSE) {
 #pragma unroll
         for (int i = 0; i < 27; ++i) {
           const double v = warp_sum((double)acc[i]);
@@ -710,6 +736,27 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           sh_red[warp][28] = q2;
           sh_cnt[warp] = nc;
         }
+        if (WPP == 1 && lane < kNumAcc) tot[lane] = sh_red[warp][lane];
+        if (WPP > 1) {
+          group_sync<WPP, NT>(g);
+          if (gtid < kNumAcc) {
+            double t = 0.0;
+            for (int w2 = 0; w2 < WPP; ++w2) t += sh_red[g * WPP + w2][gtid];
+            tot[gtid] = t;
+          }
+          if (gtid == 0)
+            for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
+        }
+      } else if (WPP == 1) {
+        const double v = warp_transpose_sum<STATS>(acc, cost, sumsq);
+        const int nc = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane < kNumAcc) tot[lane] = v;
+        if (lane == 0) sh_cnt[warp] = nc;
+      } else {
+        const double v = warp_transpose_sum<STATS>(acc, cost, sumsq);
+        const int nc = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane < kNumAcc) sh_red[warp][lane] = v;
+        if (lane == 0) sh_cnt[warp] = nc;
         group_sync<WPP, NT>(g);
         if (gtid < kNumAcc) {
           double t = 0.0;
