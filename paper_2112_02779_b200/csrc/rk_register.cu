@@ -75,6 +75,15 @@ constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
 #endif
 constexpr int kThreads = RK_ICP_THREADS;  // one CTA per pair by default (WPP = kThreads / 32)
 constexpr int kWide = 1024;               // latency-mode CTA (small batches)
+// the numpy-exact walk needs ~80 registers: at 1024 threads (64 registers)
+// it spills ~70 values in the hot loop, so its latency-mode CTAs are 512
+// threads (128 registers): one pair, cluster x8: K3 0.594 -> 0.433 ms
+// (768: 0.479 ms; scripts/latency_probe.py)
+#ifndef RK_ICP_LAT_NT_NP
+#define RK_ICP_LAT_NT_NP 512
+#endif
+template <int MATH>
+constexpr int lat_nt() { return MATH == MATH_NP ? RK_ICP_LAT_NT_NP : kWide; }
 
 struct IcpArgs {
   SensorDev s;
@@ -125,6 +134,25 @@ __device__ __noinline__ int solve_step(const double* tot, int n_corr, double* po
   return (nr < rot_eps && nt < trans_eps) ? 1 : 0;
 }
 
+// pose <- exp(xi) pose and the early-exit test, by one lane.  Out of line: its
+// own register allocation (inlined under the walk's register cap, the float64
+// temporaries live across the division / sqrt / sincos slow-path call sites
+// were spilled: ~60 local stores and reloads per update)
+__device__ __noinline__ int pose_update(double x0, double x1, double x2, double x3, double x4, double x5,
+                                        double* pose, double rot_eps, double trans_eps) {
+  const double xi[6] = {x0, x1, x2, x3, x4, x5};
+  double P[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) P[i] = pose[i];
+  se3_left_update(xi, P);
+  if (orth_defect(P) > 1e-12) reorthonormalize(P);
+#pragma unroll
+  for (int i = 0; i < 12; ++i) pose[i] = P[i];
+  const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+  const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+  return (nr < rot_eps && nt < trans_eps) ? 1 : 0;
+}
+
 // The per-iteration update (registration.py:266-282) by one warp: the common
 // case -- an SPD system whose condition number the cheap bounds already
 // settle -- runs lane-parallel in registers (right-looking Cholesky with one
@@ -150,10 +178,14 @@ __device__ __forceinline__ int warp_solve_step(const double* tot, int n_corr, do
   double a = h0;
   double pmax = 0.0, pmin = 0.0, dinv[6];
   bool ok = true;
+  // no early exit: with a break dinv[] lived in local memory (a store and a
+  // reload per pivot); after a non-positive pivot the remaining steps run on
+  // a dummy pivot and the serial path below decides
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    const double d = __shfl_sync(0xffffffffu, a, k * (k + 1) / 2 + k);
-    if (!(d > 0.0)) { ok = false; break; }
+    double d = __shfl_sync(0xffffffffu, a, k * (k + 1) / 2 + k);
+    ok = ok && d > 0.0;
+    if (!ok) d = 1.0;
     pmax = k ? fmax(pmax, d) : d;
     pmin = k ? fmin(pmin, d) : d;
     const double inv = rsqrt(d);
@@ -223,18 +255,7 @@ __device__ __forceinline__ int warp_solve_step(const double* tot, int n_corr, do
 #pragma unroll
   for (int i = 0; i < 6; ++i) xi[i] = __shfl_sync(0xffffffffu, xj, i);
   int ctrl = 0;
-  if (lane == 0) {
-    double P[12];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) P[i] = pose[i];
-    se3_left_update(xi, P);
-    if (orth_defect(P) > 1e-12) reorthonormalize(P);
-#pragma unroll
-    for (int i = 0; i < 12; ++i) pose[i] = P[i];
-    const double nr = sqrt(xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
-    const double nt = sqrt(xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
-    ctrl = (nr < rot_eps && nt < trans_eps) ? 1 : 0;
-  }
+  if (lane == 0) ctrl = pose_update(xi[0], xi[1], xi[2], xi[3], xi[4], xi[5], pose, rot_eps, trans_eps);
   return __shfl_sync(0xffffffffu, ctrl, 0);
 }
 
@@ -927,19 +948,18 @@ void allow_cluster_size() {
                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
-template <int CL>
+template <int MATH, int CL>
 int max_active_clusters() {
+  constexpr int NT = lat_nt<MATH>();
   static int cache[64] = {0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
   if (!cache[dev]) {
-    allow_cluster_size<MATH_FAST, CL>();
+    allow_cluster_size<MATH, CL, NT>();
     cudaLaunchAttribute at[1];
-    cudaLaunchConfig_t lc = cluster_config<CL>(1, nullptr, at);
+    cudaLaunchConfig_t lc = cluster_config<CL, NT>(1, nullptr, at);
     int n = 0;
-    // (occupancy of the FAST instantiation; the MATH_NP one has the same
-    // 1024-thread CTAs and register cap, so the same clusters fit)
-    if (cudaOccupancyMaxActiveClusters(&n, k_register<MATH_FAST, kWide / 32, 1, true, false, kWide, CL>, &lc) !=
+    if (cudaOccupancyMaxActiveClusters(&n, k_register<MATH, NT / 32, 1, true, false, NT, CL>, &lc) !=
             cudaSuccess || n < 1) {
       cudaGetLastError();
       n = -1;  // clusters unavailable: never chosen
@@ -995,6 +1015,7 @@ template <int MATH>
 int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) {
   constexpr int MINB = MATH == MATH_FAST ? RK_ICP_MINB : RK_ICP_MINB_NP;
   constexpr int WFULL = kThreads / 32;
+  constexpr int LNT = lat_nt<MATH>();
   const int batch = a.batch;
   // latency mode: a batch that cannot fill the GPU with 256-thread CTAs
   // (online odometry, one register() call, a short sequence) runs each pair
@@ -1016,17 +1037,17 @@ int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) 
       // the largest cluster whose batch fits in one wave of co-resident
       // clusters (B200: 1-8 pairs x8, then x4, then <= 74 x2)
       const int cl = want > 0 ? want
-                              : (batch <= max_active_clusters<8>()   ? 8
-                                 : batch <= max_active_clusters<4>() ? 4
-                                 : batch <= max_active_clusters<2>() ? 2
-                                                                     : 1);
-      if (cl == 16) return launch_cluster<MATH, 16>(a, st);
-      if (cl == 8) return launch_cluster<MATH, 8>(a, st);
-      if (cl == 4) return launch_cluster<MATH, 4>(a, st);
-      if (cl == 2) return launch_cluster<MATH, 2>(a, st);
+                              : (batch <= max_active_clusters<MATH, 8>()   ? 8
+                                 : batch <= max_active_clusters<MATH, 4>() ? 4
+                                 : batch <= max_active_clusters<MATH, 2>() ? 2
+                                                                           : 1);
+      if (cl == 16) return launch_cluster<MATH, 16, LNT>(a, st);
+      if (cl == 8) return launch_cluster<MATH, 8, LNT>(a, st);
+      if (cl == 4) return launch_cluster<MATH, 4, LNT>(a, st);
+      if (cl == 2) return launch_cluster<MATH, 2, LNT>(a, st);
     }
-    if (batch <= sm_count()) return launch<MATH, kWide / 32, 1, kWide>(a, st);
-    if (batch <= 2 * sm_count()) return launch<MATH, kWide / 64, 2, kWide / 2>(a, st);
+    if (batch <= sm_count()) return launch<MATH, LNT / 32, 1, LNT>(a, st);
+    if (batch <= 2 * sm_count()) return launch<MATH, LNT / 64, 2, LNT / 2>(a, st);
   }
   if constexpr (MATH == MATH_FAST) {  // experiment layouts (RK_ICP_WPP), FAST only
     switch (wpp) {
