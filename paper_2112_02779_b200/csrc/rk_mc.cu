@@ -72,6 +72,8 @@ __device__ __forceinline__ float2 sample(const GridView& g, const int* nb, int x
   int slot = nb[(ox * 3 + oy) * 3 + oz];
   if (slot < 0) return make_float2(0.f, 0.f);
   int lx = x - (ox - 1) * kEdge, ly = y - (oy - 1) * kEdge, lz = z - (oz - 1) * kEdge;
+  RK_DCHECK(lx >= 0 && lx < kEdge && ly >= 0 && ly < kEdge && lz >= 0 && lz < kEdge && slot < g.n_blocks,
+            "K6 corner sample", slot, (lx * kEdge + ly) * kEdge + lz);
   return g.vox[(size_t)slot * kVox + (lx * kEdge + ly) * kEdge + lz];
 }
 
@@ -205,8 +207,15 @@ __device__ int vertex_of(const GridView& g, const Mesh& m, const int* nb, int4 b
   }
   // another thread owns the key: wait for it to publish the id
   int id;
+#if RK_DEBUG_CHECKS
+  long long spins = 0;
+#endif
   while ((id = *((volatile int*)(m.vids + h))) == -1) {
+#if RK_DEBUG_CHECKS
+    RK_DCHECK(++spins < (1ll << 28), "K6 vertex publish wait", (long long)h, spins);
+#endif
   }
+  RK_DCHECK(id == -2 || (id >= 0 && id < m.vcap), "K6 vertex id", id, m.vcap);
   return id;
 }
 
@@ -277,6 +286,7 @@ __global__ void k_mc_triangles(GridView g, const int8_t* __restrict__ table, flo
       }
       if (id[0] < 0 || id[1] < 0 || id[2] < 0) continue;
       if (id[0] == id[1] || id[1] == id[2] || id[0] == id[2]) continue;
+      RK_DCHECK(id[0] < m.vcap && id[1] < m.vcap && id[2] < m.vcap, "K6 triangle vertex", id[0], m.vcap);
       // area test on the final positions (mesh_extract.py:202-209)
       const double* A = m.verts + 3 * id[0];
       const double* B = m.verts + 3 * id[1];

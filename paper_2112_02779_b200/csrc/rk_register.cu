@@ -435,6 +435,8 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
   const int col = ci * stride, row = ri * stride;
   if (row >= s.H) return;  // dropped, not clamped (registration.py:157-159)
   const int flat = row * s.W + col;
+  RK_DCHECK(pr.v >= 0 && pr.v < s.H && ci >= 0 && col < s.W && row >= 0, "K3 pixel", pr.v, col);
+  RK_DCHECK(!lvl_w || (ci < lvl_w && lvl_off + ri * lvl_w + ci >= lvl_off), "K3 level index", ci, lvl_w);
   constexpr bool FUSED = RK_ICP_FUSED && MATH == MATH_FAST;
   float4 n, q;
   if (lvl_rec && RK_SURFEL_REC == 16) {
@@ -669,6 +671,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           for (int vi = 0; vi < Hs; ++vi) {
             const float r = r_next;
             const double3 dcur = d_next;
+            RK_DCHECK(sp >= src && sp < src + HW, "K3 source walk", (long long)(sp - src), (long long)HW);
             sp += row_step;
             dp += 3 * (size_t)row_step;
             if (vi + 1 < Hs) {  // next row's range and ray, one point ahead

@@ -118,9 +118,16 @@ __device__ __forceinline__ void touch_key(const GridDev& g, int frame, long long
   bool inserted;
   long long h = hash_acquire(g, key, inserted);
   if (h < 0) { atomicExch(&g.ctr->overflow, 1); return; }
-  if (inserted) g.fresh[atomicAdd(&g.ctr->n_fresh, 1)] = (int32_t)h;
+  RK_DCHECK((unsigned long long)h <= g.hash_mask, "K4 hash slot", h, g.hash_mask);
+  if (inserted) {
+    const int fi = atomicAdd(&g.ctr->n_fresh, 1);
+    RK_DCHECK((unsigned long long)fi <= g.hash_mask, "K4 fresh list", fi, g.hash_mask);
+    g.fresh[fi] = (int32_t)h;
+  }
   if (g.h_stamp[h] != frame && atomicExch(g.h_stamp + h, frame) != frame) {
-    g.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&g.tc->n_touched), 1ull)] = (int32_t)h;
+    const unsigned long long ti = atomicAdd(reinterpret_cast<unsigned long long*>(&g.tc->n_touched), 1ull);
+    RK_DCHECK(ti <= g.hash_mask, "K4 touched list", ti, g.hash_mask);
+    g.touched[ti] = (int32_t)h;
     atomicMax(&g.tc->max_touched_key, key);
   }
 }
@@ -416,6 +423,7 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
     if (slot < 0) continue;
     const unsigned long long key = A.g.h_keys[h];
 #endif
+    RK_DCHECK(slot < A.g.cap_blocks, "K5 voxel slot", slot, A.g.cap_blocks);
     int kx, ky, kz;
     unpack_key(key, kx, ky, kz);
     double base[3];
@@ -436,6 +444,7 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
       Proj32 p = project_f32<MATH, SMEM, RK_TSDF_FAST_PROJ ? PROJ_FAST_R : PROJ_EXACT>(s, tb, x, y, z);
       int col = (int)__fadd_rn(p.u, 0.5f);
       if (col == s.W) col = 0;
+      RK_DCHECK(p.v >= 0 && p.v < s.H && col >= 0 && col < s.W, "K5 range gather", p.v, col);
       const float px = __ldg(A.range + p.v * s.W + col);
       bool ok = p.status == PROJ_OK && px > 0.0f && px >= A.cmin && px <= A.cmax && p.r <= A.cmax;
       float d = __fsub_rn(px, p.r);
