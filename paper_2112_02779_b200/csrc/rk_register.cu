@@ -352,7 +352,8 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   if (EXACT) {
     e = div_rn_fast(res, k32);
     s1 = __fadd_rn(1.0f, __fmul_rn(e, e));
-    w = div_rn_fast(1.0f, (RK_SQRT_FAST && s1 < 3.0e38f) ? sqrt_rn_normal(s1) : __fsqrt_rn(s1));  // s1 >= 1
+    w = div_rn_fast(1.0f, RK_SQRT_FAST == 2 ? sqrt_rn_normal(s1)
+                          : (RK_SQRT_FAST == 1 && s1 < 3.0e38f) ? sqrt_rn_normal(s1) : __fsqrt_rn(s1));  // s1 >= 1
   } else {
     e = res * inv_k;
     s1 = __fmaf_rn(e, e, 1.0f);
@@ -427,7 +428,8 @@ __device__ __forceinline__ void associate_moved(const SensorDev& s, const RowTab
                                                 int stride, int lvl_off, int lvl_w, float inv_s,
                                                 float gate2, float inv_k, float k32, float* acc, float& cost,
                                                 float& sumsq, int& cnt) {
-  const Proj32 pr = project_f32<MATH, SMEM, RK_ICP_ELEV_ONLY ? PROJ_NO_R : PROJ_EXACT>(s, tb, mx, my, mz);
+  constexpr int PROJ = MATH == MATH_FAST ? (RK_ICP_ELEV_ONLY ? PROJ_NO_R : PROJ_EXACT) : PROJ_EXACT_FINITE;
+  const Proj32 pr = project_f32<MATH, SMEM, PROJ>(s, tb, mx, my, mz);
   if (pr.status != PROJ_OK) return;
   int ci = (int)__fadd_rn(__fmul_rn(pr.u, inv_s), 0.5f);
   if (ci * stride >= s.W) ci = 0;

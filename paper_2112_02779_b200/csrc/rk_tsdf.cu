@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
       const float x = __fadd_rn(bx, sh_off[3 * i]);
       const float y = __fadd_rn(by, sh_off[3 * i + 1]);
       const float z = __fadd_rn(bz, sh_off[3 * i + 2]);
-      Proj32 p = project_f32<MATH, SMEM, RK_TSDF_FAST_PROJ ? PROJ_FAST_R : PROJ_EXACT>(s, tb, x, y, z);
+      Proj32 p = project_f32<MATH, SMEM, MATH != MATH_FAST ? PROJ_EXACT_FINITE : RK_TSDF_FAST_PROJ ? PROJ_FAST_R : PROJ_EXACT>(s, tb, x, y, z);
       int col = (int)__fadd_rn(p.u, 0.5f);
       if (col == s.W) col = 0;
       RK_DCHECK(p.v >= 0 && p.v < s.H && col >= 0 && col < s.W, "K5 range gather", p.v, col);
