@@ -352,7 +352,7 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   if (EXACT) {
     e = div_rn_fast(res, k32);
     s1 = __fadd_rn(1.0f, __fmul_rn(e, e));
-    w = div_rn_fast(1.0f, RK_SQRT_FAST == 2 ? sqrt_rn_normal(s1)
+    w = rcp_rn_fast(RK_SQRT_FAST == 2 ? sqrt_rn_normal(s1)
                           : (RK_SQRT_FAST == 1 && s1 < 3.0e38f) ? sqrt_rn_normal(s1) : __fsqrt_rn(s1));  // s1 >= 1
   } else {
     e = res * inv_k;
@@ -371,7 +371,7 @@ __device__ __forceinline__ void accumulate_point(float mx, float my, float mz, c
   for (int i = 0; i < 6; ++i) acc[21 + i] = __fmaf_rn(rw, J[i], acc[21 + i]);
   if (STATS) {
     if (EXACT) {
-      cost = __fadd_rn(cost, __fsub_rn(div_rn_fast(1.0f, w), 1.0f));
+      cost = __fadd_rn(cost, __fsub_rn(rcp_rn_fast(w), 1.0f));
     } else {
       // rho/k^2 = 1/w - 1 = e^2 / (sqrt(1+e^2) + 1), cancellation-free
       cost += __fdividef(e * e, __fmaf_rn(s1, w, 1.0f));
