@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(NT, RK_TSDF_CTAS_PER_SM) k_integrate(Integrate
       int col = (int)__fadd_rn(p.u, 0.5f);
       if (col == s.W) col = 0;
       RK_DCHECK(p.v >= 0 && p.v < s.H && col >= 0 && col < s.W, "K5 range gather", p.v, col);
-      const float px = __ldg(A.range + p.v * s.W + col);
+      const int pix = p.v * s.W + col;  // one 32-bit index: a single wide IMAD for the address
+      const float px = __ldg(A.range + pix);
       bool ok = p.status == PROJ_OK && px > 0.0f && px >= A.cmin && px <= A.cmax && p.r <= A.cmax;
       float d = __fsub_rn(px, p.r);
       ok = ok && d >= -A.tau;
