@@ -46,6 +46,10 @@ enum {
  * SVML sequences restated bit for bit) with exact arithmetic everywhere else:
  * the reference's projection (lidar_model.py:262-344) bit for bit. */
 enum { RK_MATH_FAST = 0, RK_MATH_CR = 1, RK_MATH_LIBM = 2, RK_MATH_NP = 3 };
+/* rk_project_f32 only (test hook): RK_MATH_NP through the finite-operand
+ * variant K3 and K5 use (branch-free square root, NaN-free clamps) -- equal
+ * to RK_MATH_NP bit for bit on finite points */
+#define RK_MATH_NP_FINITE 4
 
 /* per-pair ICP status (registration.py:266-272) */
 enum { RK_ICP_CONVERGED = 0, RK_ICP_TOO_FEW = 1, RK_ICP_DEGENERATE = 2, RK_ICP_BAD_PAIR = 3 };

@@ -127,12 +127,12 @@ extern "C" int rk_sensor_destroy(rk_sensor* s) {
 }
 
 // ------------------------------------------------------------------ projection
-template <int MATH>
+template <int MATH, int APPROX = PROJ_EXACT>
 __global__ void k_project_f32(SensorDev s, const float* __restrict__ pts, int64_t n, float* u,
                               int32_t* v, float* r, int8_t* st) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    Proj32 p = project_f32<MATH>(s, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    Proj32 p = project_f32<MATH, false, APPROX>(s, global_tables(s), pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
     if (u) u[i] = p.u;
     if (v) v[i] = p.v;
     if (r) r[i] = p.r;
@@ -176,6 +176,8 @@ extern "C" int rk_project_f32(const rk_sensor* s, const float* pts, int64_t n, i
     k_project_f32<MATH_LIBM><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   else if (math == MATH_NP)
     k_project_f32<MATH_NP><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
+  else if (math == RK_MATH_NP_FINITE)
+    k_project_f32<MATH_NP, PROJ_EXACT_FINITE><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   else
     k_project_f32<MATH_FAST><<<g, 256, 0, S(stream)>>>(s->dev, pts, n, u, v, r, status);
   RK_LAUNCHED("k_project_f32");
