@@ -201,16 +201,23 @@ int rk_make_surfel(const float* range, const float* normals, const uint8_t* vali
  * {stride, iteration, n_correspondences, cost, inlier_rmse}.
  * pt_iters (may be NULL): device counter += executed source-point-iterations
  * (the roofline work unit).  One launch; each pair runs on one
- * CTA: 256 threads for throughput batches, 512 / 1024 threads when the batch
- * has <= 2 / <= 1 pairs per SM (latency mode; RK_ICP_WIDE=0 disables it).
- * Pair indices are checked on the device against cfg->n_src_images /
- * n_dst_images (RK_ICP_BAD_PAIR). */
+ * CTA of 256 threads for throughput batches; latency mode (RK_ICP_WIDE=0
+ * disables it) runs a pair on a thread-block cluster of 16 / 8 / 4 / 2 CTAs
+ * when the batch fits one wave of such clusters (RK_ICP_CLUSTER=0|2|4|8|16
+ * forces), else on one wide CTA when the batch has <= 1 / <= 2 pairs per SM
+ * (1024 / 512 threads; 512 / 256 in RK_MATH_NP).  Pair indices are checked
+ * on the device against cfg->n_src_images / n_dst_images (RK_ICP_BAD_PAIR). */
 int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
                       const float* dst_surfel, const int32_t* pair_src,
                       const int32_t* pair_dst, int32_t batch, const double* init12,
                       const rk_icp_config* cfg, double* out12, int32_t* status,
                       int32_t* n_iters, double* stats, int32_t stats_stride,
                       unsigned long long* pt_iters, void* stream);
+
+/* diagnostic: how many thread-block clusters of cl (2, 4, 8, 16) K3 CTAs the
+ * launcher assumes co-resident for the math mode (the occupancy query it uses
+ * to pick the latency tier); -1 when unavailable */
+int rk_icp_cluster_capacity(int math, int cl);
 
 /* float64 helpers of the non-bulk registration API (registration.py:96-234):
  * pts @ R.T + t; single=False association given moved points and their

@@ -68,6 +68,7 @@ SIGNATURES = {
     "rk_make_surfel": [_p, _p, _p, _i64, _p, _p],
     "rk_register_batch": [_p, _p, _p, _p, _p, _p, _i32, _p, C.POINTER(IcpConfig), _p, _p, _p,
                           _p, _i32, _p, _p],
+    "rk_icp_cluster_capacity": [C.c_int, C.c_int],
     "rk_transform_points": [_p, _p, _i64, _p, _p],
     "rk_associate_f64": [_p, _p, _p, _p, _p, _i64, _p, _f64, _i32, _p, _p, _p, _p],
     "rk_normal_equations_f64": [_p, _p, _p, _p, _i64, _f64, _p, _p, _p],

@@ -58,6 +58,15 @@ constexpr int kNumAcc = 29;  // 21 H (upper) + 6 b + cost + sumsq
 // RK_ICP_LVL_SMEM: the per-level constants (gate^2, 1/k, 1/s, stride, surfel
 // level offset/width) live in shared memory, so under the 64-register cap the
 // compiler re-reads them with one LDS instead of re-deriving them per point
+// cluster tiers: all-to-all partials, every CTA solves its own update (one
+// cluster barrier per iteration, no pose broadcast): one pair, NP, K3 x8
+// 0.416 -> 0.372 ms, x16 0.384 -> 0.301 ms (scripts/latency_probe.py)
+#ifndef RK_ICP_CLUSTER_REDUNDANT
+#define RK_ICP_CLUSTER_REDUNDANT 1
+#endif
+#ifndef RK_ICP_CLUSTER16  // the launcher may take 16-CTA clusters (non-portable size)
+#define RK_ICP_CLUSTER16 1
+#endif
 #ifndef RK_ICP_LVL_SMEM
 #define RK_ICP_LVL_SMEM 1
 #endif
@@ -534,7 +543,12 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
   __shared__ double sh_pose[GROUPS][12];
   __shared__ double sh_red[NW][kNumAcc];
   __shared__ double sh_tot[GROUPS][kNumAcc];
-  __shared__ double sh_part[CL][kNumAcc + 1];  // CL > 1: the cluster's partials, in the lead CTA
+  // CL > 1: the cluster's partial systems.  RK_ICP_CLUSTER_REDUNDANT: every
+  // CTA receives all CL partials (double-buffered by iteration parity) and
+  // solves the update itself; otherwise the lead CTA alone receives them
+  constexpr int NPART = RK_ICP_CLUSTER_REDUNDANT ? 2 : 1;
+  __shared__ double sh_part[NPART][CL][kNumAcc + 1];
+  int parity = 0;
   __shared__ int sh_cnt[NW];
   __shared__ int sh_ctrl[GROUPS];
   __shared__ float sh_pose32[GROUPS][12];
@@ -793,7 +807,34 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           for (int w2 = 1; w2 < WPP; ++w2) sh_cnt[g * WPP] += sh_cnt[g * WPP + w2];
       }
       group_sync<WPP, NT>(g);
-      if (CL > 1) {
+      if (CL > 1 && RK_ICP_CLUSTER_REDUNDANT) {
+        // every CTA stores its partial system into slot [crank] of every
+        // CTA's buffer for this iteration's parity (posted DSMEM stores), one
+        // cluster barrier publishes them, and every CTA sums the CL partials
+        // in rank order -- the lead's sum, bit for bit -- and solves the
+        // update itself: no pose broadcast, no second barrier.  A buffer is
+        // rewritten two iterations later, after the next barrier, which no
+        // CTA passes before every CTA has read it.
+        cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        if (gtid <= kNumAcc) {
+          const double v = gtid < kNumAcc ? tot[gtid] : (double)sh_cnt[0];
+#pragma unroll
+          for (int r = 0; r < CL; ++r)
+            cl.map_shared_rank(&sh_part[parity][0][0], r)[crank * (kNumAcc + 1) + gtid] = v;
+        }
+        cl.sync();
+        if (gtid < kNumAcc) {
+          double t = sh_part[parity][0][gtid];
+          for (int r = 1; r < CL; ++r) t += sh_part[parity][r][gtid];
+          tot[gtid] = t;
+        } else if (gtid == kNumAcc) {
+          int c = (int)sh_part[parity][0][kNumAcc];
+          for (int r = 1; r < CL; ++r) c += (int)sh_part[parity][r][kNumAcc];
+          sh_cnt[0] = c;
+        }
+        parity ^= 1;
+        group_sync<WPP, NT>(g);
+      } else if (CL > 1) {
         // the cluster's partial systems -> the lead CTA: every other CTA
         // stores its partial into the lead's shared memory (posted DSMEM
         // stores, no round trips), the cluster barrier publishes them, and
@@ -801,19 +842,19 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
         cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
         if (!lead && gtid <= kNumAcc) {
           if (gtid < kNumAcc)
-            cl.map_shared_rank(&sh_part[0][0], 0)[crank * (kNumAcc + 1) + gtid] = tot[gtid];
+            cl.map_shared_rank(&sh_part[0][0][0], 0)[crank * (kNumAcc + 1) + gtid] = tot[gtid];
           else
-            cl.map_shared_rank(&sh_part[0][0], 0)[crank * (kNumAcc + 1) + kNumAcc] = (double)sh_cnt[0];
+            cl.map_shared_rank(&sh_part[0][0][0], 0)[crank * (kNumAcc + 1) + kNumAcc] = (double)sh_cnt[0];
         }
         cl.sync();
         if (lead && gtid <= kNumAcc) {
           if (gtid < kNumAcc) {
             double t = tot[gtid];
-            for (int r = 1; r < CL; ++r) t += sh_part[r][gtid];
+            for (int r = 1; r < CL; ++r) t += sh_part[0][r][gtid];
             tot[gtid] = t;
           } else {
             int c = sh_cnt[0];
-            for (int r = 1; r < CL; ++r) c += (int)sh_part[r][kNumAcc];
+            for (int r = 1; r < CL; ++r) c += (int)sh_part[0][r][kNumAcc];
             sh_cnt[0] = c;
           }
         }
@@ -822,7 +863,9 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
 #if RK_ICP_TRACE
       if (gtid == 0) printf("pair %d lv %d it %d reduced n %d\n", pair, lv, it, sh_cnt[g * WPP]);
 #endif
-      if (lead && gtid < 32) {  // the group's first warp updates the pose
+      // the group's first warp updates the pose (in a cluster: every CTA's
+      // first warp with RK_ICP_CLUSTER_REDUNDANT, else the lead's)
+      if ((lead || (CL > 1 && RK_ICP_CLUSTER_REDUNDANT)) && gtid < 32) {
         const int n_corr = sh_cnt[g * WPP];
         // (cfg fields by value: taking a kernel parameter's address would
         // spill the whole argument block to local memory)
@@ -842,7 +885,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
 #endif
         if (gtid == 0) {
           if (ctrl != 2) {
-            if (A.stats && n_done < A.stats_stride) {
+            if (lead && A.stats && n_done < A.stats_stride) {
               double* row = A.stats + ((size_t)pair * A.stats_stride + n_done) * 5;
               row[0] = stride;
               row[1] = it;
@@ -854,7 +897,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           }
           sh_ctrl[g] = ctrl;
         }
-        if (CL > 1) {
+        if (CL > 1 && !RK_ICP_CLUSTER_REDUNDANT) {
           // broadcast the pose and the control word to the other CTAs
           __syncwarp();
           cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
@@ -864,7 +907,7 @@ __global__ void __launch_bounds__(NT, MINB) k_register(IcpArgs A) {
           }
         }
       }
-      if (CL > 1)
+      if (CL > 1 && !RK_ICP_CLUSTER_REDUNDANT)
         cooperative_groups::this_cluster().sync();
       else
         group_sync<WPP, NT>(g);
@@ -1040,12 +1083,18 @@ int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) 
     const int want = fcl ? atoi(fcl) : -1;
     if (want != 0) {
       // the largest cluster whose batch fits in one wave of co-resident
-      // clusters (B200: 1-8 pairs x8, then x4, then <= 74 x2)
+      // clusters (cudaOccupancyMaxActiveClusters; B200, 512-thread CTAs:
+      // 7 x16, 15 x8, 33 x4, 74 x2), and x2 up to one pair per SM: two
+      // waves of x2 still beat one wide CTA per pair (99 pairs 1.86 vs
+      // 2.46 ms, 148: 2.17 vs 2.50; scripts/cluster_latency.py)
       const int cl = want > 0 ? want
-                              : (batch <= max_active_clusters<MATH, 8>()   ? 8
-                                 : batch <= max_active_clusters<MATH, 4>() ? 4
-                                 : batch <= max_active_clusters<MATH, 2>() ? 2
-                                                                           : 1);
+                              : (RK_ICP_CLUSTER16 && batch <= max_active_clusters<MATH, 16>() ? 16
+                                 : batch <= max_active_clusters<MATH, 8>()   ? 8
+                                 : batch <= max_active_clusters<MATH, 4>()   ? 4
+                                 : (batch <= max_active_clusters<MATH, 2>() ||
+                                    (max_active_clusters<MATH, 2>() > 0 && batch <= sm_count()))
+                                     ? 2
+                                     : 1);
       if (cl == 16) return launch_cluster<MATH, 16, LNT>(a, st);
       if (cl == 8) return launch_cluster<MATH, 8, LNT>(a, st);
       if (cl == 4) return launch_cluster<MATH, 4, LNT>(a, st);
@@ -1067,6 +1116,23 @@ int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) 
 
 }  // namespace
 
+
+// diagnostic: co-resident clusters of cl CTAs the launcher assumes (the
+// occupancy query, cached per device); -1 when clusters are unavailable
+extern "C" int rk_icp_cluster_capacity(int math, int cl) {
+  if (math == MATH_NP) {
+    if (cl == 16) return max_active_clusters<MATH_NP, 16>();
+    if (cl == 8) return max_active_clusters<MATH_NP, 8>();
+    if (cl == 4) return max_active_clusters<MATH_NP, 4>();
+    if (cl == 2) return max_active_clusters<MATH_NP, 2>();
+  } else {
+    if (cl == 16) return max_active_clusters<MATH_FAST, 16>();
+    if (cl == 8) return max_active_clusters<MATH_FAST, 8>();
+    if (cl == 4) return max_active_clusters<MATH_FAST, 4>();
+    if (cl == 2) return max_active_clusters<MATH_FAST, 2>();
+  }
+  return -1;
+}
 
 extern "C" int rk_register_batch(const rk_sensor* s, const float* src_range, const float* dst_range,
                                  const float* dst_surfel, const int32_t* pair_src,

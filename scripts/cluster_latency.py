@@ -27,10 +27,10 @@ def run(B, cl, reps=10):
     return (time.perf_counter() - t) / reps * 1e3, res
 
 
-for B in (1, 4, 8, 18, 37, 74, 99, 148):
+for B in (1, 4, 8, 9, 18, 37, 74, 99, 148):
     base_ms, base = run(B, 0)
     line = [f"B={B}: 1 CTA {base_ms:.3f} ms"]
-    for cl in (2, 4, 8, None):
+    for cl in (2, 4, 8, 16, None):
         ms, r = run(B, cl)
         dp = (r.poses - base.poses).abs().max().item()
         same = bool((r.status == base.status).all().item())

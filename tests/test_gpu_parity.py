@@ -254,9 +254,16 @@ def test_register_cr_vs_oracle(rk, pair, sensors, osensors, golden_icp):
 def test_register_batch_deterministic_and_consistent(rk, sensors, golden_icp):
     import torch
     from paper_2112_02779_b200.range_image import normals_cross_batch
+    from paper_2112_02779_b200 import _native as nat
+    from paper_2112_02779_b200.lidar_model import default_math
     g, intr = golden_icp, sensors["ouster"]
-    src = torch.from_numpy(g["street/src"]).cuda()[None].repeat(8, 1, 1)
-    dst = torch.from_numpy(g["street/dst"]).cuda()[None].repeat(8, 1, 1)
+    # a batch inside register()'s latency tier (the 16-CTA clusters when the
+    # device co-schedules several), so the per-thread split -- and every
+    # bit -- matches the single call; other tiers: the 1e-5 tier test below
+    cap16 = nat.load().rk_icp_cluster_capacity(default_math(), 16)
+    B = min(8, cap16) if cap16 >= 2 else 8
+    src = torch.from_numpy(g["street/src"]).cuda()[None].repeat(B, 1, 1)
+    dst = torch.from_numpy(g["street/dst"]).cuda()[None].repeat(B, 1, 1)
     surf = normals_cross_batch(intr, dst)
     a = rk.register_batch(intr, src, dst, surf)
     b = rk.register_batch(intr, src, dst, surf)
