@@ -304,7 +304,7 @@ def test_register_batch_index_dtypes_and_validation(rk, sensors, golden_icp):
                           inits=torch.zeros((4, 12), dtype=torch.float64))
 
 
-@pytest.mark.parametrize("batch", [1, 2, 8, 9, 17, 18, 19, 37, 38, 74, 75, 148, 149, 300])
+@pytest.mark.parametrize("batch", [1, 2, 7, 8, 9, 15, 16, 17, 18, 19, 33, 34, 37, 38, 74, 75, 148, 149, 300])
 def test_register_batch_tiers_match_register(rk, sensors, golden_icp, batch):
     """The launcher picks a cluster size (x8/x4/x2) or CTA width (1024/512/256)
     from the batch size, which changes each pair's float32 per-thread split,
@@ -381,7 +381,7 @@ def test_register_batch_layouts_match_reference(rk, wpp, sensors, golden_icp, mo
         assert rot_err(P.R, M[:3, :3]) < 1e-5 and np.linalg.norm(P.t - M[:3, 3]) < 1e-5
 
 
-@pytest.mark.parametrize("cluster", ("0", "2", "4", "8"))
+@pytest.mark.parametrize("cluster", ("0", "2", "4", "8", "16"))
 def test_register_latency_clusters_match_reference(rk, cluster, sensors, golden_icp, monkeypatch):
     """Latency mode: one pair per 1024-thread CTA (0) or per cluster of 2/4/8
     CTAs reducing through distributed shared memory -- same contract, and a
