@@ -306,7 +306,7 @@ def test_register_batch_index_dtypes_and_validation(rk, sensors, golden_icp):
 
 @pytest.mark.parametrize("batch", [1, 2, 7, 8, 9, 15, 16, 17, 18, 19, 33, 34, 37, 38, 74, 75, 148, 149, 300])
 def test_register_batch_tiers_match_register(rk, sensors, golden_icp, batch):
-    """The launcher picks a cluster size (x8/x4/x2) or CTA width (1024/512/256)
+    """The launcher picks a cluster size (x16/x8/x4/x2) or CTA width (1024/512/256; 512/256 in NP)
     from the batch size, which changes each pair's float32 per-thread split,
     so results may differ in the last bits between tiers (INTEGRATION.md,
     'Batch-size dependence').  Every tier stays inside the pose contract
@@ -383,7 +383,7 @@ def test_register_batch_layouts_match_reference(rk, wpp, sensors, golden_icp, mo
 
 @pytest.mark.parametrize("cluster", ("0", "2", "4", "8", "16"))
 def test_register_latency_clusters_match_reference(rk, cluster, sensors, golden_icp, monkeypatch):
-    """Latency mode: one pair per 1024-thread CTA (0) or per cluster of 2/4/8
+    """Latency mode: one pair per wide CTA (0) or per cluster of 2/4/8/16
     CTAs reducing through distributed shared memory -- same contract, and a
     bad pair index still yields its defined status on every cluster size."""
     import torch
