@@ -942,11 +942,44 @@ finish:
   }
 }
 
+// Shared-memory carveout: the driver's default gave the 256-thread K3 a
+// 64 KB shared configuration for its ~28 KB of CTAs (3 x 9.4 KB).  Ask for
+// just what MINB resident CTAs need (rounded up by the driver to the next
+// supported configuration), so the rest of the SM's 256 KB serves L1 and the
+// surfel gathers: NP +1.0 % (A/B x2; a 0 % hint collapses occupancy, -54 %).
+#ifndef RK_ICP_CARVEOUT
+#define RK_ICP_CARVEOUT 1
+#endif
+template <typename K>
+void set_carveout(K kernel, int ctas_per_sm) {
+  if (!RK_ICP_CARVEOUT) return;
+  cudaFuncAttributes fa;
+  int dev = 0, max_sm = 0;
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess ||
+      max_sm <= 0) {
+    cudaGetLastError();
+    return;
+  }
+  const long long need = (long long)ctas_per_sm * ((long long)fa.sharedSizeBytes + 1024);  // + reserved per CTA
+  const int pct = (int)((need * 100 + max_sm - 1) / max_sm) + 1;
+  if (pct < 100) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaGetLastError();
+}
+
 template <int MATH, int WPP, int MINB, int NT = kThreads>
 int launch(const IcpArgs& a, cudaStream_t st) {
   constexpr int GROUPS = NT / 32 / WPP;
   const unsigned grid = (unsigned)((a.batch + GROUPS - 1) / GROUPS);
   const bool smem = a.s.H <= kMaxRowsSmem && a.s.K <= kMaxInvSmem;
+  static bool carve = false;  // per instantiation (one device: the hint is per function)
+  if (!carve) {
+    set_carveout(k_register<MATH, WPP, MINB, true, true, NT>, MINB);
+    set_carveout(k_register<MATH, WPP, MINB, false, true, NT>, MINB);
+    set_carveout(k_register<MATH, WPP, MINB, true, false, NT>, MINB);
+    set_carveout(k_register<MATH, WPP, MINB, false, false, NT>, MINB);
+    carve = true;
+  }
   if (a.stats) {
     if (smem)
       k_register<MATH, WPP, MINB, true, true, NT><<<grid, NT, 0, st>>>(a);
