@@ -360,6 +360,7 @@ class _PairGraph:
         self.h_iters = t.empty((1,), dtype=t.int32, pin_memory=True)
         self.h_stats = t.empty((1, self.max_it, 5), dtype=t.float64, pin_memory=True)
         self.graph = t.cuda.CUDAGraph()
+        self._side = t.cuda.Stream()  # the fork inside the recorded graph
         side = t.cuda.Stream()
         side.wait_stream(t.cuda.current_stream())
         with t.cuda.stream(side):
@@ -372,10 +373,17 @@ class _PairGraph:
         t.cuda.current_stream().wait_stream(side)
 
     def _issue(self, intr, config):
-        self.d_src[0].copy_(self.h_src, non_blocking=True)
+        t = nat.torch()
+        main = t.cuda.current_stream()
+        # the destination first: K1 (its surfel pyramid) overlaps the source
+        # image's and the init pose's H2D, which run on a forked stream
         self.d_dst[0].copy_(self.h_dst, non_blocking=True)
-        self.d_init.copy_(self.h_init, non_blocking=True)
+        self._side.wait_stream(main)
+        with t.cuda.stream(self._side):
+            self.d_src[0].copy_(self.h_src, non_blocking=True)
+            self.d_init.copy_(self.h_init, non_blocking=True)
         self.surf = normals_cross_batch(intr, self.d_dst, strides=[s for s, _ in config.schedule])
+        main.wait_stream(self._side)
         res = register_batch(intr, self.d_src, self.d_dst, self.surf, inits=self.d_init, config=config,
                              with_stats=True)
         self.res = res
