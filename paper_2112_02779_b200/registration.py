@@ -263,7 +263,7 @@ def _pair_index(x, name: str, B: int):
 def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels=None,
                    pair_src=None, pair_dst=None, inits=None,
                    config: RegistrationConfig = RegistrationConfig(), with_stats: bool = False,
-                   math: int | None = None, pt_iters=None) -> BatchResult:
+                   math: int | None = None, pt_iters=None, out=None) -> BatchResult:
     """register() for B independent pairs in one launch (device tensors in/out).
 
     src_ranges / dst_ranges: (P, H, W) float32 CUDA tensors (image pools);
@@ -272,6 +272,8 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
     (coarse levels gather from compact decimated maps; computed if None);
     inits: (B, 12) float64 initial poses (default identity);
     pt_iters: optional (1,) int64 device counter of executed point-iterations.
+    out: optional preallocated (poses, status, iterations, stats) device
+    tensors of the result shapes (stats may be None without with_stats).
     Pair indices outside the pools are checked on the device: such pairs get
     status ICP_BAD_PAIR and their init pose.
     """
@@ -310,11 +312,22 @@ def register_batch(intr: lm.LidarIntrinsics, src_ranges, dst_ranges, dst_surfels
               and tuple(inits.shape) == (B, 12)):
         raise ValueError(f"inits must be a ({B}, 12) float64 CUDA tensor")
     inits = inits.contiguous()
-    poses = t.empty((B, 12), dtype=t.float64, device=dev)
-    status = t.empty((B,), dtype=t.int32, device=dev)
-    iters = t.empty((B,), dtype=t.int32, device=dev)
     max_it = config.max_iterations
-    stats = t.empty((B, max_it, 5), dtype=t.float64, device=dev) if with_stats else None
+    if out is not None:
+        poses, status, iters, stats = out
+        shapes = ((B, 12), (B,), (B,), (B, max_it, 5) if with_stats else None)
+        types = (t.float64, t.int32, t.int32, t.float64)
+        for x, shp, dt in zip((poses, status, iters, stats), shapes, types):
+            if shp is None:
+                continue
+            if not (nat.is_tensor(x) and x.is_cuda and x.dtype == dt and tuple(x.shape) == shp
+                    and x.is_contiguous()):
+                raise ValueError(f"out tensors must be contiguous CUDA {shapes} of {types}")
+    else:
+        poses = t.empty((B, 12), dtype=t.float64, device=dev)
+        status = t.empty((B,), dtype=t.int32, device=dev)
+        iters = t.empty((B,), dtype=t.int32, device=dev)
+        stats = t.empty((B, max_it, 5), dtype=t.float64, device=dev) if with_stats else None
     cfg = config.to_c(math)
     cfg.n_src_images, cfg.n_dst_images = int(src.shape[0]), int(dst.shape[0])
     surf = dst_surfels
@@ -355,10 +368,20 @@ class _PairGraph:
         self.d_src = nat.empty((1, H, W), np.float32)
         self.d_dst = nat.empty((1, H, W), np.float32)
         self.d_init = nat.empty((1, 12), np.float64)
-        self.h_pose = t.empty((1, 12), dtype=t.float64, pin_memory=True)
-        self.h_status = t.empty((1,), dtype=t.int32, pin_memory=True)
-        self.h_iters = t.empty((1,), dtype=t.int32, pin_memory=True)
-        self.h_stats = t.empty((1, self.max_it, 5), dtype=t.float64, pin_memory=True)
+        # pose, per-iteration stats, status, iteration count packed in one
+        # device buffer -> one D2H copy (float64 views first: 8-byte aligned)
+        n_f64 = 12 + 5 * self.max_it
+        nbytes = 8 * n_f64 + 8
+        self.d_out = t.empty((nbytes,), dtype=t.uint8, device=nat.device())
+        self.h_out = t.empty((nbytes,), dtype=t.uint8, pin_memory=True)
+        f64 = self.d_out[:8 * n_f64].view(t.float64)
+        i32 = self.d_out[8 * n_f64:].view(t.int32)
+        self.d_res = (f64[:12].view(1, 12), i32[0:1], i32[1:2], f64[12:].view(1, self.max_it, 5))
+        hf = self.h_out[:8 * n_f64].view(t.float64)
+        hi = self.h_out[8 * n_f64:].view(t.int32)
+        self.h_pose, self.h_stats = hf[:12].view(1, 12), hf[12:].view(1, self.max_it, 5)
+        self.h_status, self.h_iters = hi[0:1], hi[1:2]
+        self.d_idx = t.zeros((1,), dtype=t.int32, device=nat.device())
         self.graph = t.cuda.CUDAGraph()
         self._side = t.cuda.Stream()  # the fork inside the recorded graph
         side = t.cuda.Stream()
@@ -384,13 +407,11 @@ class _PairGraph:
             self.d_init.copy_(self.h_init, non_blocking=True)
         self.surf = normals_cross_batch(intr, self.d_dst, strides=[s for s, _ in config.schedule])
         main.wait_stream(self._side)
-        res = register_batch(intr, self.d_src, self.d_dst, self.surf, inits=self.d_init, config=config,
-                             with_stats=True)
+        res = register_batch(intr, self.d_src, self.d_dst, self.surf, pair_src=self.d_idx,
+                             pair_dst=self.d_idx, inits=self.d_init, config=config, with_stats=True,
+                             out=self.d_res)
         self.res = res
-        self.h_pose.copy_(res.poses, non_blocking=True)
-        self.h_status.copy_(res.status, non_blocking=True)
-        self.h_iters.copy_(res.iterations, non_blocking=True)
-        self.h_stats.copy_(res.stats, non_blocking=True)
+        self.h_out.copy_(self.d_out, non_blocking=True)
 
     def run(self, src: np.ndarray, dst: np.ndarray, init_row12: np.ndarray):
         t = nat.torch()
