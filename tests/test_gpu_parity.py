@@ -273,6 +273,29 @@ def test_register_batch_deterministic_and_consistent(rk, sensors, golden_icp):
     assert np.array_equal(a.pose(0).matrix(), single.pose.matrix())
 
 
+def test_register_batch_preallocated_outputs(rk, sensors, golden_icp):
+    """register_batch(out=...) writes into the caller's tensors (the latency
+    graph's packed buffer) with the same bits, and rejects wrong shapes."""
+    import torch
+    g, intr = golden_icp, sensors["ouster"]
+    src = torch.from_numpy(g["street/src"]).cuda()[None]
+    dst = torch.from_numpy(g["street/dst"]).cuda()[None]
+    cfg = rk.RegistrationConfig()
+    ref = rk.register_batch(intr, src, dst, config=cfg, with_stats=True)
+    out = (torch.empty((1, 12), dtype=torch.float64, device="cuda"),
+           torch.empty((1,), dtype=torch.int32, device="cuda"),
+           torch.empty((1,), dtype=torch.int32, device="cuda"),
+           torch.empty((1, cfg.max_iterations, 5), dtype=torch.float64, device="cuda"))
+    res = rk.register_batch(intr, src, dst, config=cfg, with_stats=True, out=out)
+    assert res.poses is out[0] and torch.equal(out[0], ref.poses)
+    assert torch.equal(out[1], ref.status) and torch.equal(out[2], ref.iterations)
+    n = int(ref.iterations[0])
+    assert torch.equal(out[3][:, :n], ref.stats[:, :n])
+    bad = (out[0].float(),) + out[1:]
+    with pytest.raises(ValueError):
+        rk.register_batch(intr, src, dst, config=cfg, with_stats=True, out=bad)
+
+
 def test_register_batch_index_dtypes_and_validation(rk, sensors, golden_icp):
     """int64 pair indices (torch's default) give the same poses as int32 ones
     (the converted copies stay alive across the launch), and host-side or
