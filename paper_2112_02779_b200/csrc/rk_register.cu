@@ -1117,13 +1117,15 @@ int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) 
     if (want != 0) {
       // the largest cluster whose batch fits in one wave of co-resident
       // clusters (cudaOccupancyMaxActiveClusters; B200, 512-thread CTAs:
-      // 7 x16, 15 x8, 33 x4, 74 x2), and x2 up to one pair per SM: two
-      // waves of x2 still beat one wide CTA per pair (99 pairs 1.86 vs
-      // 2.46 ms, 148: 2.17 vs 2.50; scripts/cluster_latency.py)
+      // 7 x16, 15 x8, 33 x4, 74 x2); x4 up to two such waves (the query is
+      // conservative for x4 -- 37 pairs ran in one wave, 0.86 ms against
+      // x2's 1.40 -- and even two waves of x4 beat x2), and x2 up to one
+      // pair per SM: two waves of x2 still beat one wide CTA per pair (99
+      // pairs 1.86 vs 2.46 ms, 148: 2.17 vs 2.50; scripts/cluster_latency.py)
       const int cl = want > 0 ? want
                               : (RK_ICP_CLUSTER16 && batch <= max_active_clusters<MATH, 16>() ? 16
                                  : batch <= max_active_clusters<MATH, 8>()   ? 8
-                                 : batch <= max_active_clusters<MATH, 4>()   ? 4
+                                 : batch <= 2 * max_active_clusters<MATH, 4>() ? 4
                                  : (batch <= max_active_clusters<MATH, 2>() ||
                                     (max_active_clusters<MATH, 2>() > 0 && batch <= sm_count()))
                                      ? 2

@@ -27,7 +27,7 @@ def run(B, cl, reps=10):
     return (time.perf_counter() - t) / reps * 1e3, res
 
 
-for B in (1, 4, 8, 9, 18, 37, 74, 99, 148):
+for B in (1, 4, 8, 9, 18, 33, 37, 50, 66, 67, 74, 99, 148):
     base_ms, base = run(B, 0)
     line = [f"B={B}: 1 CTA {base_ms:.3f} ms"]
     for cl in (2, 4, 8, 16, None):
