@@ -1119,15 +1119,17 @@ int launch_tiers(const IcpArgs& a, cudaStream_t st, const char* force, int wpp) 
       // clusters (cudaOccupancyMaxActiveClusters; B200, 512-thread CTAs:
       // 7 x16, 15 x8, 33 x4, 74 x2); x4 up to two such waves (the query is
       // conservative for x4 -- 37 pairs ran in one wave, 0.86 ms against
-      // x2's 1.40 -- and even two waves of x4 beat x2), and x2 up to one
-      // pair per SM: two waves of x2 still beat one wide CTA per pair (99
-      // pairs 1.86 vs 2.46 ms, 148: 2.17 vs 2.50; scripts/cluster_latency.py)
+      // x2's 1.40 -- and even two waves of x4 beat x2), and x2 up to 2.75
+      // pairs per SM: its waves still beat one wide CTA per pair or the
+      // throughput kernel (99 pairs 1.86 vs 2.46 ms, 149: 2.17 vs 4.00,
+      // 296: 3.97 vs 4.52, 400: 4.90 vs 5.12; at 444 the throughput kernel
+      // wins, 5.53 vs 5.72; scripts/cluster_latency.py, tier_probe.py)
       const int cl = want > 0 ? want
                               : (RK_ICP_CLUSTER16 && batch <= max_active_clusters<MATH, 16>() ? 16
                                  : batch <= max_active_clusters<MATH, 8>()   ? 8
                                  : batch <= 2 * max_active_clusters<MATH, 4>() ? 4
                                  : (batch <= max_active_clusters<MATH, 2>() ||
-                                    (max_active_clusters<MATH, 2>() > 0 && batch <= sm_count()))
+                                    (max_active_clusters<MATH, 2>() > 0 && 4 * batch <= 11 * sm_count()))
                                      ? 2
                                      : 1);
       if (cl == 16) return launch_cluster<MATH, 16, LNT>(a, st);
