@@ -18,6 +18,9 @@ pool = scenes.pair_pool_poses(256, seed=0)
 src = pipeline.render_batch(intr, scenes.street_scene(), [b @ g for b, g in pool])
 dst = pipeline.render_batch(intr, scenes.street_scene(), [b for b, _ in pool])
 cfg = rk.RegistrationConfig()
+if len(sys.argv) > 1 and sys.argv[1] == "fast":  # the FAST kernels' crossovers
+    from paper_2112_02779_b200 import lidar_model as lm
+    lm.set_default_math(lm.MATH_FAST)
 surf = normals_cross_batch(intr, dst, strides=[s for s, _ in cfg.schedule])
 
 
